@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 NNM hot path (BASELINE.json metric on its headline config).
+
+Workload (default ``--config c4``): generate_synthetic(2_000_000, 25, 4000, 1.0,
+seed=5) -- BASELINE config 4, the metric's quoted shape -- clustered to the full
+single-linkage dendrogram (euclidean, no constraints).  One *step* = one full
+clustering run (all Boruvka rounds: fused FP32 screening scans, FP64 exact
+keys, hooking, sort + replay of the 1,999,999 merges).
+
+* ``value``   distance-pair evaluations per second over the step, inputs already
+              resident in HBM (a DeviceDataset built before the timed region).
+* ``e2e``     the same metric through the public API (``engine.run``) with host
+              buffers: float64 X uploaded, merge log + labels read back, every step.
+* ``roofline`` dominant kernel = the fused screening scan; algorithmic flops per
+              launch = n(n-1)/2 pairs x 3d flops (sub, mul, add per coordinate),
+              average launch time from CUDA events on the library's stream, peak =
+              FFMA2 microbenchmark on this GPU (libnnm nnm_measure_fp32_peak).
+* ``cpu_baseline`` the C oracle (a port of the reference's round scan) on the
+              host cores, one top-P round on a bounded row sample.
+
+``--impl reference`` times the reference's CPU path (the oracle port: there is
+no compiled reference, the reference is pure Python + scipy) on the same
+metric/config, rank 0 only.
+
+Multi-GPU (torchrun): one rank per GPU, the tile-pair space is partitioned
+and two all-reduce(MIN) calls per round combine the per-row keys
+(paper_1402_3789_b200.distributed); ``scaling`` is strong (fixed problem).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": ("c1: 10k x 8, 5 blobs, unconstrained euclidean", {}),
+    "c3": ("c3: 500k x 25, 1000 blobs, dmax=5.0", {"dmax": 5.0}),
+    "c4": ("c4: 2M x 25, 4000 blobs (spread 1, seed 5), euclidean full dendrogram", {}),
+}
+METRIC = "NNM clustering distance-pair evaluations/s (BASELINE: 2Mx25 NNM clustering; pairs/s vs FP32 roofline)"
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(X, seconds_target: float = 12.0) -> dict:
+    """Oracle port (C, all host threads) timed on one top-P round over a row sample."""
+    from oracle import nnm_oracle as orc
+
+    threads = os.cpu_count() or 1
+    d = X.shape[1]
+
+    def one(m):
+        S = np.ascontiguousarray(X[:: max(1, X.shape[0] // m)][:m])
+        roots = np.arange(m, dtype=np.int64)
+        sizes = np.ones(m, dtype=np.int64)
+        t0 = time.perf_counter()
+        orc.top_p(S, roots, sizes, 256, threads=threads)
+        return time.perf_counter() - t0
+
+    m = 4000
+    t = one(m)
+    rate = m * (m - 1) / 2 / t
+    m = int(min(X.shape[0], max(4000, (2 * rate * seconds_target) ** 0.5)))
+    t = one(m)
+    pairs = m * (m - 1) / 2
+    return {"value": pairs / t, "unit": "pairs/s", "cores": threads, "kind": "port",
+            "sample": f"one reference round (top-P=256 selection over all {pairs:.3g} pairs) on a "
+                      f"{m}-row strided sample of the {X.shape[0]}x{d} input; {t:.1f} s",
+            "seconds": t}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    from paper_1402_3789_b200.datagen import config_dataset
+
+    X = config_dataset(args.config)
+    samples = []
+    for step in range(args.warmup + args.steps):
+        cb = cpu_baseline(X, seconds_target=args.ref_seconds)
+        if step >= args.warmup:
+            samples.append(cb)
+    v = statistics.median(s["value"] for s in samples)
+    last = samples[-1]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(s["seconds"] for s in samples),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": CONFIGS[args.config][0], "n": X.shape[0],
+                                        "d": X.shape[1]},
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": last["cores"], "kind": "port",
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _load_traffic():
+    p = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            return None
+    return None
+
+
+def run_gpu(args) -> None:
+    import ctypes
+
+    import torch
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    os.environ["NNM_DEVICE"] = str(local)
+    import paper_1402_3789_b200 as nnm
+    from paper_1402_3789_b200 import _native
+    from paper_1402_3789_b200.datagen import config_dataset
+    from paper_1402_3789_b200.engine import run_arrays
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    desc, cons_kw = CONFIGS[args.config]
+    X = config_dataset(args.config)
+    n, d = X.shape
+    cons = nnm.ConstraintSet(**cons_kw)
+    lib = _native.load()
+    pairs_full = n * (n - 1) / 2
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- device-resident step
+    ddata = _native.DeviceDataset(X, device=local)
+
+    def step_device():
+        if dist is None:
+            out = run_arrays(ddata, cons, 256, nnm.MetricKind.EUCLIDEAN)
+            return out[5]
+        from paper_1402_3789_b200.distributed import run_boruvka_distributed_handle
+
+        return run_boruvka_distributed_handle(ddata, dmax=cons.dmax)[4]
+
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    stats = []
+    with ClockSampler(local) as clk:
+        barrier()
+        t_wall = time.perf_counter()
+        ev0.record()
+        for _ in range(args.steps):
+            stats.append(step_device())
+        ev1.record()
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    # the step is host-orchestrated (host syncs between kernels), so the CUDA-event
+    # span on torch's stream brackets all of the library's work on its own stream
+    ms_dev = max(ev0.elapsed_time(ev1), 1e3 * t_wall) / args.steps
+    ms_dev = max_over_ranks(ms_dev)
+    pairs_step = sum_over_ranks(sum(s["pairs_evaluated"] for s in stats) / args.steps)
+    value = pairs_step / (ms_dev / 1e3)
+    scan_ms = sum(s["scan_ms"] for s in stats)
+    scans = sum(s["scans"] for s in stats)
+    launches = int(sum(s["kernel_launches"] for s in stats))
+    clocks = clk.summary()
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if dist is None:
+        Xh = torch.from_numpy(X).pin_memory().numpy()
+        e2e_ms = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = nnm.run(nnm.Dataset(values=Xh), nnm.RunConfig(constraints=cons))
+            _ = res.merges.array["dist"].sum() + res.assignments.sum()
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+        pe = res.device_stats["pairs_evaluated"]
+        e2e = {"value": pe / (statistics.mean(e2e_ms) / 1e3), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(X.nbytes),
+               "d2h_bytes_per_step": int(res.merges.array.nbytes + res.assignments.nbytes),
+               "ms_per_step": statistics.mean(e2e_ms), "api": "paper_1402_3789_b200.run"}
+
+    peak = ctypes.c_double()
+    _native.check(lib.nnm_measure_fp32_peak(local, ctypes.byref(peak)))
+    avg_launch_ms = scan_ms / max(scans, 1)
+    # algorithmic flops of one full-range scan launch (per rank: its share of tile pairs)
+    flops_launch = (sum(s["pairs_evaluated"] for s in stats) / max(scans, 1)) * 3 * d
+    achieved = flops_launch / (avg_launch_ms / 1e3) / 1e12
+    roofline = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                "frac": achieved / peak.value if peak.value else None, "traffic": _load_traffic(),
+                "kernel": "scan_rows_kernel (fused FP32 distance + eligibility + per-row top-2)",
+                "peak_source": "measured FFMA2 microbenchmark on this GPU (MEASURED_PEAKS.json has no FP32 entry)",
+                "avg_launch_ms": avg_launch_ms,
+                "scan_share_of_step": scan_ms / (ms_dev * args.steps)}
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    cb = cpu_baseline(X) if world == 1 and not args.no_cpu_baseline else None
+    cfg = {"workload": desc, "n": n, "d": d, "metric": "euclidean", "pairs_per_step": pairs_step,
+           "l2": "inputs larger than L2 (X32 %.0f MB + X64 %.0f MB > 126 MB)" % (n * d * 4 / 1e6, X.nbytes / 1e6),
+           "seconds_to_dendrogram": ms_dev / 1e3, "boruvka_rounds": stats[-1]["boruvka_rounds"],
+           "merges": n - 1, "parallelism": f"tile-pair shards x{world}" if world > 1 else "1 GPU"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32-screen+f64-exact",
+        "data": "synthetic (generate_synthetic, bit-identical to the reference generator)",
+        "config": cfg, "e2e": e2e, "roofline": roofline, "cpu_baseline": cb,
+        "clocks": clocks, "gpu_launches": launches,
+        "device_stats": stats[-1],
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * nnm.h -- C ABI of the B200-native NNM (constrained single-linkage) hot path.
+ *
+ * The reference (parclust, arXiv 1402.3789 restated in Python) has no formal
+ * plugin registry: its seams are module attributes that its own tests patch
+ * (SURVEY.md 8b).  Each entry point below replaces one of them; the citation
+ * gives the reference interface (paths relative to
+ * /root/reference/pkg/src/parclust/).  Bindings a maintainer adds on the
+ * reference side are shown in INTEGRATION.md.
+ *
+ * Conventions (mirroring the reference):
+ *   - metric: 0 euclidean, 1 squared-euclidean, 2 manhattan, 3 chebyshev
+ *     (metrics.py:34-53).  Distances are "internal" units (squared for both
+ *     euclidean kinds) except nnm_merge.dist, which is reported units
+ *     (metrics.py:86-90).
+ *   - integer constraints < 0 mean unset; dmax / thr NaN means unset
+ *     (model.py:190-218).
+ *   - return 0 on success, a negative NNM_E_* code otherwise; the message is
+ *     available from nnm_last_error() (thread-local).  NNM_E_INVALID maps to
+ *     the reference's ValidationError (model.py:25-26); NNM_E_CUDA to
+ *     WorkerError (scheduler.py:45-46).
+ *   - all pointers are caller-owned host memory unless the name says _dev.
+ *   - there is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point returns NNM_E_CUDA.
+ */
+#ifndef NNM_H
+#define NNM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NNM_ABI_VERSION 1
+
+enum {
+  NNM_OK = 0,
+  NNM_E_INVALID = -1,     /* ValidationError */
+  NNM_E_CUDA = -2,        /* device / kernel failure (WorkerError) */
+  NNM_E_UNSUPPORTED = -3, /* input outside the implemented envelope */
+  NNM_E_NOMEM = -4,       /* device allocation failed */
+  NNM_E_CAPACITY = -5     /* caller buffer too small */
+};
+
+enum { NNM_EUCLIDEAN = 0, NNM_SQEUCLIDEAN = 1, NNM_MANHATTAN = 2, NNM_CHEBYSHEV = 3 };
+
+/* stop reasons (engine.py:146-151, :174-176) */
+enum { NNM_STOP_KL1 = 1, NNM_STOP_NO_ELIGIBLE = 2, NNM_STOP_SINGLE_CLUSTER = 3 };
+
+/* nnm_run flags */
+enum {
+  NNM_FLAG_ROUNDS = 1 /* force the exact top-P round path (engine.py:154-199) for every
+                         constraint set, so rounds / round_counters match the reference */
+};
+
+/* algorithm actually used by nnm_run (stats.path) */
+enum { NNM_PATH_NONE = 0, NNM_PATH_BORUVKA = 1, NNM_PATH_ROUNDS = 2 };
+
+typedef struct nnm_dataset nnm_dataset; /* opaque: X resident in HBM (FP64 + FP32 tiles) */
+
+typedef struct { /* ConstraintSet, model.py:190-218 */
+  int64_t kl1, kl2, kl3, kl4;
+  double dmax;
+} nnm_constraints;
+
+typedef struct { /* MergeEvent, model.py:221-238 (step = array index) */
+  int64_t round, root_a, root_b;
+  double dist;
+  int64_t new_size, point_a, point_b;
+} nnm_merge;
+
+typedef struct { /* engine.py:187-190 */
+  int64_t round, selected, merged, same_root, kl2, kl3, unprocessed;
+} nnm_round_counters;
+
+typedef struct {
+  int32_t path;            /* NNM_PATH_* */
+  int32_t device;
+  int64_t scans;           /* full screening scans launched */
+  double pairs_evaluated;  /* unordered pairs evaluated by the FP32 screen */
+  double scan_ms;          /* CUDA-event time of all screening-scan launches */
+  double total_ms;         /* wall time of the call */
+  int64_t ambiguous_rows;  /* rows re-resolved exactly (FP32 margin too small) */
+  int64_t exact_evals;     /* FP64 pair evaluations */
+  int64_t boruvka_rounds;
+  int64_t kernel_launches; /* libnnm kernels launched by the call (library sorts excluded) */
+} nnm_stats;
+
+int nnm_abi_version(void);
+const char *nnm_last_error(void);
+int nnm_device_count(int32_t *out);
+
+/* Upload X (n x d, row-major float64, finite) to `device` and build the FP32
+ * screening tiles.  Replaces Dataset's array being read by every scan task
+ * (model.py:29-76; pairgen.py:247-298).  Validation as Dataset.__post_init__. */
+int nnm_dataset_create(const double *X, int64_t n, int32_t d, int32_t device, nnm_dataset **out);
+/* Same, with X already resident in device memory on `device` (copied internally). */
+int nnm_dataset_create_device(const double *X_dev, int64_t n, int32_t d, int32_t device,
+                              nnm_dataset **out);
+int nnm_dataset_destroy(nnm_dataset *ds);
+
+/* Round seam: replaces scheduler.run_round / pairgen.global_top_p
+ * (scheduler.py:268-335, pairgen.py:319-324).  roots/sizes are the
+ * EligibilitySnapshot arrays (pairgen.py:134-166), thr its threshold in internal
+ * units (NaN = none).  Writes the <=P smallest eligible pairs ascending by
+ * (dist, a, b) into out_* (capacity P) and their count into out_len; the result
+ * is bit-identical to global_top_p. */
+int nnm_top_p(nnm_dataset *ds, int32_t metric, const int64_t *roots, const int64_t *sizes,
+              double thr, int64_t kl2, int64_t kl3, int64_t P, double *out_dist, int64_t *out_a,
+              int64_t *out_b, int64_t *out_len);
+
+/* Run seam: replaces engine.run (engine.py:154-199).  out_merges has capacity
+ * n-1, out_assign n, out_counters counters_cap entries (NULL allowed).
+ * Without kl4 the merge list (root_a, root_b, dist, new_size, point_a, point_b)
+ * equals the reference's for any P; with kl4 (or NNM_FLAG_ROUNDS) the round
+ * structure, `round` fields and counters are reproduced as well. */
+int nnm_run(nnm_dataset *ds, int32_t metric, const nnm_constraints *cons, int64_t P,
+            int32_t flags, nnm_merge *out_merges, int64_t *out_n_merges, int64_t *out_assign,
+            int64_t *out_rounds, int32_t *out_stop, nnm_round_counters *out_counters,
+            int64_t counters_cap, int64_t *out_n_counters, nnm_stats *stats);
+
+/* Metric seam: internal distances of every (x_i, y_j), FP64 bit-identical to
+ * metrics.internal_pairwise (metrics.py:67-73).  out is nx*ny row-major. */
+int nnm_pairwise(int32_t metric, const double *x, int64_t nx, const double *y, int64_t ny,
+                 int32_t d, int32_t device, double *out);
+
+/* ---- staged Boruvka API for the multi-GPU driver (paper_1402_3789_b200.distributed) ----
+ * One process per GPU; every rank holds the full dataset.  Per round each rank
+ * scans its share of the upper-triangular tile pairs into (B1, B2), the driver
+ * combines the per-row keys across ranks with two all-reduce(min) calls, and
+ * every rank then finishes the round identically.  Device buffers are
+ * caller-owned (e.g. torch tensors) of n uint64 each. */
+int nnm_bv_begin(nnm_dataset *ds, int32_t metric, double dmax, int64_t *out_tile_pairs);
+int nnm_bv_scan(nnm_dataset *ds, int64_t w_begin, int64_t w_end, uint64_t *B1_dev,
+                uint64_t *B2_dev);
+/* B2 contribution for the global second-best: B2c[i] = (B1loc[i] == B1glob[i]) ? B2loc[i] : B1loc[i] */
+int nnm_bv_second(nnm_dataset *ds, const uint64_t *B1loc_dev, const uint64_t *B2loc_dev,
+                  const uint64_t *B1glob_dev, uint64_t *B2c_dev);
+/* finish a round from the global keys; *out_edges = MST edges added (0: converged) */
+int nnm_bv_finish_round(nnm_dataset *ds, const uint64_t *B1_dev, const uint64_t *B2_dev,
+                        int64_t *out_edges);
+/* sort + replay the accumulated edges into the merge log (kl1 truncation) */
+int nnm_bv_end(nnm_dataset *ds, int64_t kl1, nnm_merge *out_merges, int64_t *out_n_merges,
+               int64_t *out_assign, int64_t *out_rounds, int32_t *out_stop, nnm_stats *stats);
+
+/* ---- diagnostics ----
+ * Sustained FP32 (FFMA2) throughput of `device` in TFLOP/s: the roofline
+ * denominator for the screening scan, which runs on the FP32 pipe. */
+int nnm_measure_fp32_peak(int32_t device, double *tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNM_H */

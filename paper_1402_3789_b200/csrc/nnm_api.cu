@@ -1,0 +1,1292 @@
+// nnm_api.cu -- C ABI, dataset residency, FP64 exact kernels, Boruvka and
+// top-P round orchestration for the B200 NNM hot path.
+//
+// Reference mapping (paths relative to /root/reference/pkg/src/parclust/):
+//   nnm_dataset_create  <- model.Dataset (model.py:29-76)
+//   nnm_top_p           <- scheduler.run_round / pairgen.global_top_p
+//                          (scheduler.py:268-335, pairgen.py:247-324)
+//   nnm_run             <- engine.run (engine.py:154-199) incl. order_batch
+//                          (:73-87) and process_batch (:90-143)
+//   nnm_pairwise        <- metrics.internal_pairwise (metrics.py:67-73)
+// The paper's CPU "managers" (scheduler.py:268-335) become one stream per
+// dataset: kernels are queued back to back and the host only syncs to read
+// counts that size the next launch.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/nnm.h"
+#include "nnm_common.cuh"
+#include "nnm_kernels.cuh"
+
+using namespace nnm;
+
+// ----------------------------------------------------------------------------
+// errors
+// ----------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+
+struct NnmError {
+  int code;
+  std::string msg;
+};
+
+#define CUDA_TRY(x)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      throw NnmError{e_ == cudaErrorMemoryAllocation ? NNM_E_NOMEM : NNM_E_CUDA,          \
+                     std::string(#x) + " failed: " + cudaGetErrorString(e_)};             \
+  } while (0)
+
+[[noreturn]] void invalid(const std::string& m) { throw NnmError{NNM_E_INVALID, m}; }
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return NNM_OK;
+  } catch (const NnmError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = std::string("internal error: ") + e.what();
+    return NNM_E_CUDA;
+  }
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t c = count > 0 ? count : 1;
+    CUDA_TRY(cudaMalloc(&p, c * sizeof(T)));
+    n = c;
+  }
+};
+
+std::atomic<int64_t> g_launches{0};  // libnnm kernel launches (process-wide)
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+inline int blocks_for(int64_t n, int t = 256) { return (int)std::max<int64_t>(1, (n + t - 1) / t); }
+
+inline double bits_to_double(unsigned long long b) {
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+}
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// small kernels
+// ----------------------------------------------------------------------------
+namespace nnm {
+
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return (unsigned long long)__double_as_longlong(x);
+}
+__device__ __forceinline__ double bitsd(unsigned long long b) {
+  return __longlong_as_double((long long)b);
+}
+
+// X64 (row-major) -> X32 SoA [d][ld] rounded to nearest, +inf padding.
+__global__ void prepare_kernel(const double* __restrict__ X64, int64_t n, int d, int64_t ld,
+                               float* __restrict__ X32, int* range_err) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ld) return;
+  for (int k = 0; k < d; ++k) {
+    float v = INFINITY;
+    if (i < n) {
+      double x = X64[i * d + k];
+      if (!(fabs(x) <= 1e18)) atomicExch(range_err, 1);
+      v = __double2float_rn(x);
+    }
+    X32[(int64_t)k * ld + i] = v;
+  }
+}
+
+// per-point norm in the metric's norm, rounded up; global max via atomicMax on bits
+__global__ void norms_kernel(const double* __restrict__ X64, int64_t n, int d, int metric,
+                             double* __restrict__ norm, unsigned long long* maxbits) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* x = X64 + i * d;
+  double s = 0.0;
+  if (metric == EUCLIDEAN || metric == SQEUCLIDEAN) {
+    for (int k = 0; k < d; ++k) s += x[k] * x[k];
+    s = sqrt(s) * (1.0 + 1e-12) + 1e-300;
+  } else if (metric == MANHATTAN) {
+    for (int k = 0; k < d; ++k) s += fabs(x[k]);
+    s = s * (1.0 + 1e-12) + 1e-300;
+  } else {
+    for (int k = 0; k < d; ++k) s = fmax(s, fabs(x[k]));
+    s = s * (1.0 + 1e-12) + 1e-300;
+  }
+  norm[i] = s;
+  atomicMax(maxbits, dbits(s));
+}
+
+template <int M>
+__global__ void pairwise_kernel(const double* __restrict__ X, int64_t nx,
+                                const double* __restrict__ Y, int64_t ny, int d,
+                                double* __restrict__ out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nx * ny) return;
+  int64_t i = t / ny, j = t % ny;
+  out[t] = exact_dist<M>(X + i * d, Y + j * d, d);
+}
+
+template <int M>
+__global__ void exact_pairs_kernel(const double* __restrict__ X64, int d,
+                                   const int2* __restrict__ pairs, int64_t count,
+                                   double* __restrict__ out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  int2 p = pairs[t];
+  out[t] = exact_dist<M>(X64 + (int64_t)p.x * d, X64 + (int64_t)p.y * d, d);
+}
+
+__global__ void fill_comp_kernel(int* comp, int* psize, int64_t n, int64_t ld) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ld) return;
+  comp[i] = i < n ? (int)i : -1;
+  if (psize) psize[i] = i < n ? 1 : 0;
+}
+
+// Boruvka refine: exact FP64 key of each row's screened best partner, and
+// certification against the screened second best.
+template <int M>
+__global__ void refine_kernel(const double* __restrict__ X64, int n, int d,
+                              const unsigned long long* __restrict__ B1,
+                              const unsigned long long* __restrict__ B2,
+                              const double* __restrict__ norm, double maxnorm, ErrModel em,
+                              double thr, unsigned long long* rb_d, int* rb_j, double* rowlow,
+                              int* amb, unsigned long long* amb_count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long k1 = B1[i];
+  if (!key_valid(k1)) {
+    rb_d[i] = NONE_KEY;
+    rb_j[i] = -1;
+    rowlow[i] = INFINITY;
+    return;
+  }
+  int j = (int)key_index(k1);
+  double e = exact_dist<M>(X64 + (int64_t)i * d, X64 + (int64_t)j * d, d);
+  double R = norm[i] + maxnorm;
+  rowlow[i] = exact_lower(em, (double)key_value(k1), R);
+  unsigned long long k2 = B2[i];
+  double low2 = key_valid(k2) ? exact_lower(em, (double)key_value(k2), R) : INFINITY;
+  if (e <= thr) {
+    rb_d[i] = dbits(e);
+    rb_j[i] = j;
+    if (low2 > e) return;  // certified: every other partner is strictly farther
+  } else {
+    rb_d[i] = NONE_KEY;
+    rb_j[i] = -1;
+    if (low2 > thr) return;  // certified: no eligible partner at all
+  }
+  unsigned long long pos = atomicAdd(amb_count, 1ull);
+  amb[pos] = i;
+}
+
+__global__ void compmin_d_kernel(int n, const int* __restrict__ comp,
+                                 const unsigned long long* __restrict__ rb_d,
+                                 unsigned long long* cmin_d) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long v = rb_d[i];
+  if (v != NONE_KEY) atomicMin(cmin_d + comp[i], v);
+}
+
+__global__ void compmin_ab_kernel(int n, const int* __restrict__ comp,
+                                  const unsigned long long* __restrict__ rb_d,
+                                  const int* __restrict__ rb_j,
+                                  const unsigned long long* __restrict__ cmin_d,
+                                  unsigned long long* cmin_ab) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long v = rb_d[i];
+  int c = comp[i];
+  if (v == NONE_KEY || v != cmin_d[c]) return;
+  unsigned a = (unsigned)min(i, rb_j[i]), b = (unsigned)max(i, rb_j[i]);
+  atomicMin(cmin_ab + c, ((unsigned long long)a << 32) | b);
+}
+
+// ambiguous rows that could still hold their component's minimum
+__global__ void amb_filter_kernel(const int* __restrict__ amb, int na, const int* __restrict__ comp,
+                                  const double* __restrict__ rowlow,
+                                  const unsigned long long* __restrict__ cmin_d,
+                                  const unsigned long long* __restrict__ rb_d, double thr,
+                                  const double* __restrict__ norm, double maxnorm, ErrModel em,
+                                  int* out, float* bound, unsigned long long* count) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= na) return;
+  int i = amb[t];
+  unsigned long long cb = cmin_d[comp[i]];
+  double cm = cb == NONE_KEY ? INFINITY : bitsd(cb);
+  if (!(rowlow[i] <= cm)) return;
+  double e = rb_d[i] == NONE_KEY ? INFINITY : bitsd(rb_d[i]);
+  double lim = fmin(e, thr);
+  unsigned long long pos = atomicAdd(count, 1ull);
+  out[pos] = i;
+  bound[pos] = float_up(screen_upper(em, lim, norm[i] + maxnorm));
+}
+
+// gather rows (global ids) into a SoA block [d][ldr]
+__global__ void gather_kernel(const float* __restrict__ X32, int64_t ld, int d,
+                              const int* __restrict__ ids, int nr, int64_t ldr,
+                              float* __restrict__ out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ldr) return;
+  int g = t < nr ? ids[t] : -1;
+  for (int k = 0; k < d; ++k) out[(int64_t)k * ldr + t] = g >= 0 ? X32[(int64_t)k * ld + g] : INFINITY;
+}
+
+__global__ void reset_rows_kernel(const int* __restrict__ rows, int nr, unsigned long long* rb_d,
+                                  int* rb_j) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nr) return;
+  rb_d[rows[t]] = NONE_KEY;
+  rb_j[rows[t]] = 0x7FFFFFFF;
+}
+
+__global__ void rowmin_d_kernel(const int2* __restrict__ pairs, const double* __restrict__ dv,
+                                int64_t count, double thr, unsigned long long* rb_d) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  if (dv[t] <= thr) atomicMin(rb_d + pairs[t].x, dbits(dv[t]));
+}
+
+__global__ void rowmin_j_kernel(const int2* __restrict__ pairs, const double* __restrict__ dv,
+                                int64_t count, double thr, const unsigned long long* rb_d,
+                                int* rb_j) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  int2 p = pairs[t];
+  if (dv[t] <= thr && dbits(dv[t]) == rb_d[p.x]) atomicMin(rb_j + p.x, p.y);
+}
+
+__global__ void fix_rows_kernel(const int* __restrict__ rows, int nr,
+                                const unsigned long long* rb_d, int* rb_j) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nr) return;
+  if (rb_d[rows[t]] == NONE_KEY) rb_j[rows[t]] = -1;
+}
+
+struct Edge {
+  double d;
+  int a, b;
+  int round;
+  int pad;
+};
+
+struct EdgeLess {
+  __host__ __device__ bool operator()(const Edge& x, const Edge& y) const {
+    if (x.d != y.d) return x.d < y.d;
+    if (x.a != y.a) return x.a < y.a;
+    return x.b < y.b;
+  }
+};
+
+__global__ void hook_kernel(int n, const int* __restrict__ comp,
+                            const unsigned long long* __restrict__ cmin_d,
+                            const unsigned long long* __restrict__ cmin_ab, int* parent,
+                            Edge* edges, unsigned long long* edge_count, int round) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n || comp[c] != c) return;
+  unsigned long long e = cmin_ab[c];
+  if (e == NONE_KEY) {
+    parent[c] = c;
+    return;
+  }
+  int a = (int)(e >> 32), b = (int)(e & 0xFFFFFFFFull);
+  int ca = comp[a], cb = comp[b];
+  int other = (ca == c) ? cb : ca;
+  bool mutual = (cmin_ab[other] == e);
+  bool record = !mutual || c < other;
+  parent[c] = (mutual && c < other) ? c : other;
+  if (record) {
+    unsigned long long pos = atomicAdd(edge_count, 1ull);
+    Edge ed;
+    ed.d = bitsd(cmin_d[c]);
+    ed.a = a;
+    ed.b = b;
+    ed.round = round;
+    ed.pad = 0;
+    edges[pos] = ed;
+  }
+}
+
+__global__ void jump_kernel(int n, const int* __restrict__ comp, int* parent, int* changed) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n || comp[c] != c) return;
+  int p = parent[c];
+  int pp = parent[p];
+  if (p != pp) {
+    parent[c] = pp;
+    *changed = 1;
+  }
+}
+
+__global__ void relabel_kernel(int n, int* comp, const int* __restrict__ parent) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  comp[i] = parent[comp[i]];
+}
+
+// ---- round path -----------------------------------------------------------
+struct Cand {
+  double d;
+  int a, b;
+};
+struct CandLess {
+  __host__ __device__ bool operator()(const Cand& x, const Cand& y) const {
+    if (x.d != y.d) return x.d < y.d;
+    if (x.a != y.a) return x.a < y.a;
+    return x.b < y.b;
+  }
+};
+
+// distinct row-best pairs with exact keys (an upper bound for the P-th key)
+template <int M>
+__global__ void rowpairs_kernel(const double* __restrict__ X64, int n, int d,
+                                const unsigned long long* __restrict__ B1, double thr, Cand* out,
+                                unsigned long long* count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long k = B1[i];
+  if (!key_valid(k)) return;
+  int j = (int)key_index(k);
+  if (!(i < j)) {
+    unsigned long long kj = B1[j];
+    if (key_valid(kj) && (int)key_index(kj) == i) return;  // emitted by row j
+  }
+  double e = exact_dist<M>(X64 + (int64_t)i * d, X64 + (int64_t)j * d, d);
+  if (!(e <= thr)) return;
+  unsigned long long pos = atomicAdd(count, 1ull);
+  Cand c;
+  c.d = e;
+  c.a = min(i, j);
+  c.b = max(i, j);
+  out[pos] = c;
+}
+
+__global__ void active_rows_kernel(int n, const unsigned long long* __restrict__ B1,
+                                   const double* __restrict__ norm, double maxnorm, ErrModel em,
+                                   double tau, int* out, unsigned long long* count) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long k = B1[i];
+  if (!key_valid(k)) return;
+  if (exact_lower(em, (double)key_value(k), norm[i] + maxnorm) <= tau) {
+    unsigned long long pos = atomicAdd(count, 1ull);
+    out[pos] = i;
+  }
+}
+
+__global__ void pairs_to_cands_kernel(const int2* __restrict__ pairs, const double* __restrict__ dv,
+                                      int64_t count, double lim, Cand* out,
+                                      unsigned long long* n_out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  if (!(dv[t] <= lim)) return;
+  unsigned long long pos = atomicAdd(n_out, 1ull);
+  Cand c;
+  c.d = dv[t];
+  c.a = pairs[t].x;
+  c.b = pairs[t].y;
+  out[pos] = c;
+}
+
+__global__ void snapshot_update_kernel(int n, int* comp, int* psize, const int* __restrict__ rmap,
+                                       const int* __restrict__ rsize) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = rmap[comp[i]];
+  comp[i] = c;
+  psize[i] = rsize[c];
+}
+
+__global__ void scatter_kernel(const int2* __restrict__ kv, int cnt, int* arr) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < cnt) arr[kv[t].x] = kv[t].y;
+}
+
+__global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void iota_kernel(int* a, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+__global__ void ones_kernel(int* a, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = 1;
+}
+
+}  // namespace nnm
+
+// ----------------------------------------------------------------------------
+// dataset handle
+// ----------------------------------------------------------------------------
+struct nnm_dataset {
+  std::mutex mu;
+  int device = 0;
+  int64_t n = 0;
+  int d = 0;
+  int64_t ld = 0;  // n_pad
+  int T = 0;
+  int sms = 148;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  DevBuf<double> X64;
+  DevBuf<float> X32;
+  int norm_metric = -1;
+  DevBuf<double> norm;
+  double maxnorm = 0.0;
+  DevBuf<unsigned long long> scratch_u64;
+
+  DevBuf<int> comp, psize;
+  DevBuf<unsigned long long> B1, B2;
+  // boruvka
+  int bv_metric = 0;
+  double bv_thr = INFINITY;
+  float bv_thr_hi = INFINITY;
+  ErrModel em{};
+  int bv_round = 0;
+  int64_t bv_ncomp = 0;
+  DevBuf<unsigned long long> rb_d;
+  DevBuf<int> rb_j;
+  DevBuf<double> rowlow;
+  DevBuf<int> amb, resc, parent;
+  DevBuf<float> resc_bound, gathered;
+  DevBuf<unsigned long long> cmin_d, cmin_ab, counters;
+  DevBuf<Edge> edges;
+  DevBuf<int2> pairs;
+  DevBuf<double> pair_d;
+  DevBuf<int> flag;
+  // round path
+  DevBuf<Cand> cands, cands2;
+  DevBuf<int> active, rmap, rsize;
+  DevBuf<int2> kv;
+  nnm_stats stats{};
+  std::vector<float> scan_ms_pending;
+
+  ~nnm_dataset() {
+    if (st) {
+      cudaSetDevice(device);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+
+  void sync() { CUDA_TRY(cudaStreamSynchronize(st)); }
+
+  // key arrays start at NONE_KEY (INT64_MAX: signed and unsigned min agree, so
+  // NCCL / gloo int64 all-reduce(MIN) combines them correctly)
+  void fill_none(unsigned long long* p, int64_t cnt) {
+    fill_u64_kernel<<<blocks_for(cnt), 256, 0, st>>>(p, cnt, NONE_KEY); note_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
+
+  template <class T>
+  T read1(const T* dev) {
+    T v;
+    CUDA_TRY(cudaMemcpyAsync(&v, dev, sizeof(T), cudaMemcpyDeviceToHost, st));
+    sync();
+    return v;
+  }
+
+  void ensure_norms(int metric) {
+    int kind = (metric == SQEUCLIDEAN) ? EUCLIDEAN : metric;
+    if (norm_metric == kind) return;
+    norm.ensure(n);
+    scratch_u64.ensure(4);
+    CUDA_TRY(cudaMemsetAsync(scratch_u64.p, 0, sizeof(unsigned long long), st));
+    norms_kernel<<<blocks_for(n), 256, 0, st>>>(X64.p, n, d, kind, norm.p, scratch_u64.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    maxnorm = bits_to_double(read1(scratch_u64.p));
+    norm_metric = kind;
+  }
+
+  int64_t tile_pairs() const { return (int64_t)T * (T + 1) / 2; }
+
+  // full or partial screening scan into (b1, b2); times the launch with events
+  void scan(int metric, unsigned long long* b1, unsigned long long* b2, bool top2, int kl2, int kl3,
+            float thr_hi, int64_t w_begin, int64_t w_end) {
+    fill_none(b1, n);
+    if (b2) fill_none(b2, n);
+    ScanArgs a;
+    a.X32 = X32.p;
+    a.ld = ld;
+    a.n = (int)n;
+    a.d = d;
+    a.T = T;
+    a.comp = comp.p;
+    a.psize = psize.p ? psize.p : comp.p;
+    a.kl2 = kl2;
+    a.kl3 = kl3;
+    a.thr_hi = thr_hi;
+    a.w_begin = w_begin;
+    a.w_end = w_end;
+    a.B1 = b1;
+    a.B2 = b2;
+    int occ = scan_occupancy(metric, d);
+    int64_t items = w_end - w_begin;
+    int grid = (int)std::min<int64_t>(items, (int64_t)sms * occ);
+    if (grid < 1) return;
+    CUDA_TRY(cudaEventRecord(ev0, st));
+    CUDA_TRY(launch_scan(metric, a, top2, grid, st));
+    note_launch();
+    CUDA_TRY(cudaEventRecord(ev1, st));
+    CUDA_TRY(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+    stats.scan_ms += ms;
+    stats.scans += 1;
+    // unordered real pairs covered by this work range
+    stats.pairs_evaluated += (double)n * (double)(n - 1) / 2.0 * ((double)items / (double)tile_pairs());
+  }
+
+  // collect pairs (row list x columns) with screened value <= per-row bound
+  int64_t collect(int metric, const int* rows, int nr, const float* bounds, const int* cols,
+                  int nc_cols, int triangle, int kl2, int kl3) {
+    if (nr <= 0 || nc_cols <= 0) return 0;
+    int64_t ldr = ((int64_t)nr + TILE - 1) / TILE * TILE;
+    gathered.ensure((size_t)ldr * d);
+    gather_kernel<<<blocks_for(ldr), 256, 0, st>>>(X32.p, ld, d, rows, nr, ldr, gathered.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    const float* XC = X32.p;
+    int64_t ldc = ld;
+    DevBuf<float> gcols;
+    if (cols) {
+      ldc = ((int64_t)nc_cols + TILE - 1) / TILE * TILE;
+      if (cols == rows) {
+        XC = gathered.p;
+        ldc = ldr;
+      } else {
+        gcols.ensure((size_t)ldc * d);
+        gather_kernel<<<blocks_for(ldc), 256, 0, st>>>(X32.p, ld, d, cols, nc_cols, ldc, gcols.p); note_launch();
+        CUDA_TRY(cudaGetLastError());
+        XC = gcols.p;
+      }
+    }
+    counters.ensure(8);
+    unsigned long long cap = std::max<unsigned long long>(pairs.n, 1u << 16);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      pairs.ensure(cap);
+      CUDA_TRY(cudaMemsetAsync(counters.p + 6, 0, sizeof(unsigned long long), st));
+      CollectArgs a;
+      a.XR = gathered.p;
+      a.ldr = ldr;
+      a.nr = nr;
+      a.rid = rows;
+      a.XC = XC;
+      a.ldc = ldc;
+      a.nc = nc_cols;
+      a.cid = cols;
+      a.d = d;
+      a.comp = comp.p;
+      a.psize = psize.p ? psize.p : comp.p;
+      a.kl2 = kl2;
+      a.kl3 = kl3;
+      a.rbound = bounds;
+      a.triangle = triangle;
+      a.out = pairs.p;
+      a.count = counters.p + 6;  // [0..2] boruvka, [3..5] top-P
+      a.cap = pairs.n;
+      int64_t items = (ldr / TILE) * (ldc / TILE);
+      int grid = (int)std::min<int64_t>(items, (int64_t)sms * 2);
+      CUDA_TRY(launch_collect(metric, a, grid, st));
+      note_launch();
+      unsigned long long cnt = read1(counters.p + 6);
+      if (cnt <= pairs.n) return (int64_t)cnt;
+      cap = cnt + (cnt >> 2);
+    }
+    throw NnmError{NNM_E_CUDA, "collect: candidate buffer overflow after resize"};
+  }
+
+  void exact_pairs(int metric, int64_t count) {
+    pair_d.ensure(count);
+    if (count == 0) return;
+    switch (metric) {
+      case MANHATTAN:
+        exact_pairs_kernel<MANHATTAN><<<blocks_for(count), 256, 0, st>>>(X64.p, d, pairs.p, count, pair_d.p); note_launch();
+        break;
+      case CHEBYSHEV:
+        exact_pairs_kernel<CHEBYSHEV><<<blocks_for(count), 256, 0, st>>>(X64.p, d, pairs.p, count, pair_d.p); note_launch();
+        break;
+      default:
+        exact_pairs_kernel<EUCLIDEAN><<<blocks_for(count), 256, 0, st>>>(X64.p, d, pairs.p, count, pair_d.p); note_launch();
+    }
+    CUDA_TRY(cudaGetLastError());
+    stats.exact_evals += count;
+  }
+
+  // ---------------------------------------------------------------- Boruvka
+  void bv_begin(int metric, double dmax) {
+    bv_metric = metric;
+    ensure_norms(metric);
+    em = make_err_model(metric, d);
+    bv_thr = INFINITY;
+    bv_thr_hi = INFINITY;
+    if (!std::isnan(dmax)) {
+      bv_thr = metric == EUCLIDEAN ? dmax * dmax : dmax;  // metrics.py:93-103
+      bv_thr_hi = float_up(screen_upper(em, bv_thr, 2.0 * maxnorm));
+    }
+    comp.ensure(ld);
+    fill_comp_kernel<<<blocks_for(ld), 256, 0, st>>>(comp.p, nullptr, n, ld); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    rb_d.ensure(n);
+    rb_j.ensure(n);
+    rowlow.ensure(n);
+    amb.ensure(n);
+    resc.ensure(n);
+    resc_bound.ensure(n);
+    parent.ensure(n);
+    cmin_d.ensure(n);
+    cmin_ab.ensure(n);
+    counters.ensure(8);
+    edges.ensure(std::max<int64_t>(n - 1, 1));
+    flag.ensure(1);
+    CUDA_TRY(cudaMemsetAsync(counters.p, 0, 8 * sizeof(unsigned long long), st));
+    bv_round = 0;
+    bv_ncomp = n;
+  }
+
+  template <int M>
+  void refine_t(const unsigned long long* b1, const unsigned long long* b2) {
+    refine_kernel<M><<<blocks_for(n), 256, 0, st>>>(X64.p, (int)n, d, b1, b2, norm.p, maxnorm, em,
+                                                    bv_thr, rb_d.p, rb_j.p, rowlow.p, amb.p,
+                                                    counters.p + 1); note_launch();
+  }
+
+  int64_t bv_finish_round(const unsigned long long* b1, const unsigned long long* b2) {
+    const int N = (int)n;
+    ++bv_round;
+    // counters[0]: edges (cumulative), [1]: ambiguous, [2]: rescan rows
+    CUDA_TRY(cudaMemsetAsync(counters.p + 1, 0, 2 * sizeof(unsigned long long), st));
+    switch (bv_metric) {
+      case MANHATTAN: refine_t<MANHATTAN>(b1, b2); break;
+      case CHEBYSHEV: refine_t<CHEBYSHEV>(b1, b2); break;
+      default: refine_t<EUCLIDEAN>(b1, b2);
+    }
+    CUDA_TRY(cudaGetLastError());
+    fill_none(cmin_d.p, n);
+    compmin_d_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, rb_d.p, cmin_d.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long n_amb = read1(counters.p + 1);
+    stats.ambiguous_rows += (int64_t)n_amb;
+    if (n_amb > 0) {
+      amb_filter_kernel<<<blocks_for(n_amb), 256, 0, st>>>(amb.p, (int)n_amb, comp.p, rowlow.p,
+                                                         cmin_d.p, rb_d.p, bv_thr, norm.p, maxnorm,
+                                                         em, resc.p, resc_bound.p, counters.p + 2); note_launch();
+      CUDA_TRY(cudaGetLastError());
+      unsigned long long n_res = read1(counters.p + 2);
+      if (n_res > 0) {
+        int64_t np = collect(bv_metric, resc.p, (int)n_res, resc_bound.p, nullptr, N, 0, INT_UNSET,
+                             INT_UNSET);
+        reset_rows_kernel<<<blocks_for(n_res), 256, 0, st>>>(resc.p, (int)n_res, rb_d.p, rb_j.p); note_launch();
+        exact_pairs(bv_metric, np);
+        if (np > 0) {
+          rowmin_d_kernel<<<blocks_for(np), 256, 0, st>>>(pairs.p, pair_d.p, np, bv_thr, rb_d.p); note_launch();
+          rowmin_j_kernel<<<blocks_for(np), 256, 0, st>>>(pairs.p, pair_d.p, np, bv_thr, rb_d.p,
+                                                          rb_j.p); note_launch();
+        }
+        fix_rows_kernel<<<blocks_for(n_res), 256, 0, st>>>(resc.p, (int)n_res, rb_d.p, rb_j.p); note_launch();
+        CUDA_TRY(cudaGetLastError());
+        // recompute component minima with the resolved rows
+        fill_none(cmin_d.p, n);
+        compmin_d_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, rb_d.p, cmin_d.p); note_launch();
+      }
+    }
+    fill_none(cmin_ab.p, n);
+    compmin_ab_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, rb_d.p, rb_j.p, cmin_d.p, cmin_ab.p); note_launch();
+    unsigned long long before = read1(counters.p);
+    hook_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, cmin_d.p, cmin_ab.p, parent.p, edges.p,
+                                               counters.p, bv_round); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    for (int it = 0; it < 64; ++it) {
+      CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+      jump_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, parent.p, flag.p); note_launch();
+      CUDA_TRY(cudaGetLastError());
+      if (read1(flag.p) == 0) break;
+    }
+    relabel_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, parent.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long after = read1(counters.p);
+    int64_t added = (int64_t)(after - before);
+    bv_ncomp -= added;
+    stats.boruvka_rounds = bv_round;
+    return added;
+  }
+
+  // sort edges by (d, a, b) and replay them through a min-root union-find
+  void bv_end(int64_t kl1, nnm_merge* out, int64_t* n_merges, int64_t* assign, int64_t* rounds,
+              int32_t* stop) {
+    unsigned long long ne = read1(counters.p);
+    std::vector<Edge> h(ne);
+    if (ne > 0) {
+      thrust::sort(thrust::cuda::par.on(st), edges.p, edges.p + ne, EdgeLess());
+      CUDA_TRY(cudaMemcpyAsync(h.data(), edges.p, ne * sizeof(Edge), cudaMemcpyDeviceToHost, st));
+      sync();
+    }
+    // union-find replay (model.py:109-187): union keeps the smaller root
+    std::vector<int64_t> par(n), sz(n, 1);
+    for (int64_t i = 0; i < n; ++i) par[i] = i;
+    auto find = [&](int64_t x) {
+      int64_t r = x;
+      while (par[r] != r) r = par[r];
+      while (par[x] != r) {
+        int64_t nx = par[x];
+        par[x] = r;
+        x = nx;
+      }
+      return r;
+    };
+    int64_t count = n, nm = 0;
+    auto stop_of = [&](int64_t c) -> int {
+      if (c == 1) return NNM_STOP_SINGLE_CLUSTER;
+      if (kl1 >= 0 && c <= kl1) return NNM_STOP_KL1;
+      return 0;
+    };
+    int reason = stop_of(count);
+    int64_t max_round = 0;
+    if (!reason) {
+      for (unsigned long long t = 0; t < ne; ++t) {
+        const Edge& e = h[t];
+        int64_t ra = find(e.a), rb = find(e.b);
+        if (ra == rb) throw NnmError{NNM_E_CUDA, "boruvka produced a cycle (internal error)"};
+        int64_t keep = std::min(ra, rb), drop = std::max(ra, rb);
+        par[drop] = keep;
+        sz[keep] += sz[drop];
+        --count;
+        nnm_merge& m = out[nm++];
+        m.round = e.round;
+        m.root_a = keep;
+        m.root_b = drop;
+        m.dist = bv_metric == EUCLIDEAN ? std::sqrt(e.d) : e.d;  // metrics.py:86-90
+        m.new_size = sz[keep];
+        m.point_a = e.a;
+        m.point_b = e.b;
+        max_round = std::max<int64_t>(max_round, e.round);
+        reason = stop_of(count);
+        if (reason) break;
+      }
+      if (!reason) reason = NNM_STOP_NO_ELIGIBLE;
+    }
+    for (int64_t i = 0; i < n; ++i) assign[i] = find(i);
+    *n_merges = nm;
+    *rounds = (n > 1 && stop_of(n) == 0) ? bv_round : 0;
+    *stop = reason;
+  }
+
+  // ---------------------------------------------------------------- top-P
+  // Exact top-P eligible pairs for the current (comp, psize) snapshot.
+  template <int M>
+  void rowpairs_t(double thr, unsigned long long* cnt) {
+    rowpairs_kernel<M><<<blocks_for(n), 256, 0, st>>>(X64.p, (int)n, d, B1.p, thr, cands.p, cnt); note_launch();
+  }
+
+  void top_p(int metric, double thr, int kl2, int kl3, int64_t P, std::vector<Cand>& out) {
+    ensure_norms(metric);
+    em = make_err_model(metric, d);
+    float thr_hi = std::isinf(thr) ? INFINITY : float_up(screen_upper(em, thr, 2.0 * maxnorm));
+    B1.ensure(n);
+    scan(metric, B1.p, nullptr, false, kl2, kl3, thr_hi, 0, tile_pairs());
+    counters.ensure(8);
+    cands.ensure(n);
+    CUDA_TRY(cudaMemsetAsync(counters.p + 3, 0, 3 * sizeof(unsigned long long), st));
+    switch (metric) {
+      case MANHATTAN: rowpairs_t<MANHATTAN>(thr, counters.p + 3); break;
+      case CHEBYSHEV: rowpairs_t<CHEBYSHEV>(thr, counters.p + 3); break;
+      default: rowpairs_t<EUCLIDEAN>(thr, counters.p + 3);
+    }
+    CUDA_TRY(cudaGetLastError());
+    int64_t nc = (int64_t)read1(counters.p + 3);
+    stats.exact_evals += nc;
+    double tau = INFINITY;
+    if (nc >= P) {
+      thrust::sort(thrust::cuda::par.on(st), cands.p, cands.p + nc, CandLess());
+      Cand c = read1(cands.p + (P - 1));
+      tau = c.d;
+    }
+    active.ensure(n);
+    active_rows_kernel<<<blocks_for(n), 256, 0, st>>>((int)n, B1.p, norm.p, maxnorm, em, tau,
+                                                      active.p, counters.p + 4); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    int64_t na = (int64_t)read1(counters.p + 4);
+    out.clear();
+    if (na < 2) return;
+    // deterministic order of the active set (atomics appended in arbitrary order)
+    thrust::sort(thrust::cuda::par.on(st), active.p, active.p + na);
+    double lim = std::min(tau, thr);
+    float bound = float_up(screen_upper(em, lim, 2.0 * maxnorm));
+    DevBuf<float> bnd;
+    bnd.ensure(na);
+    std::vector<float> hb(na, bound);
+    CUDA_TRY(cudaMemcpyAsync(bnd.p, hb.data(), na * sizeof(float), cudaMemcpyHostToDevice, st));
+    int64_t np = collect(metric, active.p, (int)na, bnd.p, active.p, (int)na, 1, kl2, kl3);
+    exact_pairs(metric, np);
+    cands2.ensure(std::max<int64_t>(np, 1));
+    CUDA_TRY(cudaMemsetAsync(counters.p + 5, 0, sizeof(unsigned long long), st));
+    if (np > 0)
+      pairs_to_cands_kernel<<<blocks_for(np), 256, 0, st>>>(pairs.p, pair_d.p, np, lim, cands2.p,
+                                                            counters.p + 5); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    int64_t nk = (int64_t)read1(counters.p + 5);
+    if (nk == 0) return;
+    thrust::sort(thrust::cuda::par.on(st), cands2.p, cands2.p + nk, CandLess());
+    int64_t take = std::min<int64_t>(nk, P);
+    out.resize(take);
+    CUDA_TRY(cudaMemcpyAsync(out.data(), cands2.p, take * sizeof(Cand), cudaMemcpyDeviceToHost, st));
+    sync();
+  }
+};
+
+// ----------------------------------------------------------------------------
+// validation helpers (model.py:29-76, :190-218; engine.py:48-54)
+// ----------------------------------------------------------------------------
+namespace {
+void check_metric(int32_t metric) {
+  if (metric < 0 || metric > 3)
+    invalid("unknown metric code " + std::to_string(metric) +
+            "; choose one of: euclidean, squared-euclidean, manhattan, chebyshev");
+}
+
+void check_constraints(const nnm_constraints* c) {
+  const char* names[4] = {"kl1", "kl2", "kl3", "kl4"};
+  int64_t v[4] = {c->kl1, c->kl2, c->kl3, c->kl4};
+  for (int i = 0; i < 4; ++i)
+    if (v[i] == 0) invalid(std::string(names[i]) + " must be a positive count, got 0");
+  if (c->kl2 >= 1 && c->kl3 >= 1 && !(c->kl3 > c->kl2))
+    invalid("kl3 must exceed kl2, got kl3=" + std::to_string(c->kl3) + " kl2=" + std::to_string(c->kl2));
+  if (!std::isnan(c->dmax) && !(c->dmax >= 0.0))
+    invalid("dmax must be nonnegative, got " + std::to_string(c->dmax));
+}
+
+int clamp_int(int64_t v) { return v < 0 ? INT_UNSET : (int)std::min<int64_t>(v, INT_UNSET - 1); }
+
+void init_device(int32_t device, int* sms) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw NnmError{NNM_E_CUDA, "no CUDA device available (libnnm has no CPU fallback)"};
+  if (device < 0 || device >= count) invalid("device index out of range");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    throw NnmError{NNM_E_CUDA, std::string("libnnm is built for sm_100a; device is ") + prop.name};
+  *sms = prop.multiProcessorCount;
+}
+
+nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d, int32_t device) {
+  if (n < 1 || d < 1)
+    invalid("dataset must have at least 1 point and 1 feature, got " + std::to_string(n) + "x" +
+            std::to_string(d));
+  if (n >= (int64_t)1 << 31) throw NnmError{NNM_E_UNSUPPORTED, "n must be < 2^31"};
+  if (!on_device) {
+    for (int64_t i = 0; i < n * d; ++i)
+      if (!std::isfinite(X[i])) invalid("non-finite feature value in row " + std::to_string(i / d + 1));
+  }
+  int sms = 0;
+  init_device(device, &sms);
+  auto* ds = new nnm_dataset();
+  try {
+    ds->device = device;
+    ds->sms = sms;
+    ds->n = n;
+    ds->d = d;
+    ds->ld = (n + TILE - 1) / TILE * TILE;
+    ds->T = (int)(ds->ld / TILE);
+    CUDA_TRY(cudaStreamCreateWithFlags(&ds->st, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreate(&ds->ev0));
+    CUDA_TRY(cudaEventCreate(&ds->ev1));
+    if ((size_t)ds->d * TILE * 2 * sizeof(float) + 8192 > 200 * 1024)
+      throw NnmError{NNM_E_UNSUPPORTED, "d too large for the shared-memory tile (d <= 190)"};
+    ds->X64.ensure((size_t)n * d);
+    CUDA_TRY(cudaMemcpyAsync(ds->X64.p, X, (size_t)n * d * sizeof(double),
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ds->st));
+    ds->X32.ensure((size_t)ds->ld * d);
+    ds->flag.ensure(1);
+    CUDA_TRY(cudaMemsetAsync(ds->flag.p, 0, sizeof(int), ds->st));
+    prepare_kernel<<<blocks_for(ds->ld), 256, 0, ds->st>>>(ds->X64.p, n, d, ds->ld, ds->X32.p,
+                                                          ds->flag.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    int range_err = ds->read1(ds->flag.p);
+    if (range_err)
+      throw NnmError{NNM_E_UNSUPPORTED,
+                     "feature magnitude above 1e18 is outside the FP32 screening range"};
+  } catch (...) {
+    delete ds;
+    throw;
+  }
+  return ds;
+}
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// C ABI
+// ----------------------------------------------------------------------------
+extern "C" {
+
+int nnm_abi_version(void) { return NNM_ABI_VERSION; }
+
+const char* nnm_last_error(void) { return g_err.c_str(); }
+
+int nnm_device_count(int32_t* out) {
+  return guarded([&] {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    *out = (e == cudaSuccess) ? c : 0;
+  });
+}
+
+int nnm_dataset_create(const double* X, int64_t n, int32_t d, int32_t device, nnm_dataset** out) {
+  return guarded([&] {
+    if (!X || !out) invalid("null argument");
+    *out = make_dataset(X, false, n, d, device);
+  });
+}
+
+int nnm_dataset_create_device(const double* X_dev, int64_t n, int32_t d, int32_t device,
+                              nnm_dataset** out) {
+  return guarded([&] {
+    if (!X_dev || !out) invalid("null argument");
+    *out = make_dataset(X_dev, true, n, d, device);
+  });
+}
+
+int nnm_dataset_destroy(nnm_dataset* ds) {
+  return guarded([&] { delete ds; });
+}
+
+int nnm_pairwise(int32_t metric, const double* x, int64_t nx, const double* y, int64_t ny,
+                 int32_t d, int32_t device, double* out) {
+  return guarded([&] {
+    check_metric(metric);
+    if (nx < 0 || ny < 0 || d < 1) invalid("bad shape");
+    if (nx == 0 || ny == 0) return;
+    int sms;
+    init_device(device, &sms);
+    DevBuf<double> dx, dy, dout;
+    dx.ensure(nx * d);
+    dy.ensure(ny * d);
+    dout.ensure(nx * ny);
+    CUDA_TRY(cudaMemcpy(dx.p, x, nx * d * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dy.p, y, ny * d * sizeof(double), cudaMemcpyHostToDevice));
+    int64_t tot = nx * ny;
+    switch (metric) {
+      case MANHATTAN: pairwise_kernel<MANHATTAN><<<blocks_for(tot), 256>>>(dx.p, nx, dy.p, ny, d, dout.p); note_launch(); break;
+      case CHEBYSHEV: pairwise_kernel<CHEBYSHEV><<<blocks_for(tot), 256>>>(dx.p, nx, dy.p, ny, d, dout.p); note_launch(); break;
+      default: pairwise_kernel<EUCLIDEAN><<<blocks_for(tot), 256>>>(dx.p, nx, dy.p, ny, d, dout.p); note_launch();
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(out, dout.p, tot * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int nnm_top_p(nnm_dataset* ds, int32_t metric, const int64_t* roots, const int64_t* sizes,
+              double thr, int64_t kl2, int64_t kl3, int64_t P, double* out_dist, int64_t* out_a,
+              int64_t* out_b, int64_t* out_len) {
+  return guarded([&] {
+    if (!ds) invalid("null dataset");
+    if (P < 1) invalid("P must be at least 1, got " + std::to_string(P));  // pairgen.py:256-257
+    check_metric(metric);
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    const int64_t n = ds->n;
+    std::vector<int> hc(ds->ld, -1), hs(ds->ld, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (roots[i] < 0 || roots[i] >= n) invalid("root label out of range");
+      hc[i] = (int)roots[i];
+      hs[i] = (int)std::min<int64_t>(sizes[i], INT_UNSET - 1);
+    }
+    ds->comp.ensure(ds->ld);
+    ds->psize.ensure(ds->ld);
+    CUDA_TRY(cudaMemcpyAsync(ds->comp.p, hc.data(), ds->ld * sizeof(int), cudaMemcpyHostToDevice, ds->st));
+    CUDA_TRY(cudaMemcpyAsync(ds->psize.p, hs.data(), ds->ld * sizeof(int), cudaMemcpyHostToDevice, ds->st));
+    std::vector<Cand> res;
+    ds->top_p(metric, std::isnan(thr) ? INFINITY : thr, clamp_int(kl2), clamp_int(kl3), P, res);
+    for (size_t t = 0; t < res.size(); ++t) {
+      out_dist[t] = res[t].d;
+      out_a[t] = res[t].a;
+      out_b[t] = res[t].b;
+    }
+    *out_len = (int64_t)res.size();
+  });
+}
+
+int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_t P, int32_t flags,
+            nnm_merge* out_merges, int64_t* out_n_merges, int64_t* out_assign, int64_t* out_rounds,
+            int32_t* out_stop, nnm_round_counters* out_counters, int64_t counters_cap,
+            int64_t* out_n_counters, nnm_stats* stats) {
+  return guarded([&] {
+    if (!ds || !cons) invalid("null argument");
+    check_metric(metric);
+    check_constraints(cons);
+    if (P < 1) invalid("pairs_per_batch must be at least 1, got " + std::to_string(P));
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t launches0 = g_launches.load();
+    ds->stats = nnm_stats{};
+    ds->stats.device = ds->device;
+    const int64_t n = ds->n;
+    const bool rounds_path = (flags & NNM_FLAG_ROUNDS) || cons->kl2 > 0 || cons->kl3 > 0 || cons->kl4 > 0;
+    int64_t n_counters = 0;
+    if (!rounds_path) {
+      // ---------------- Boruvka: exact MST of the eligible graph, then replay
+      ds->stats.path = NNM_PATH_BORUVKA;
+      ds->bv_begin(metric, cons->dmax);
+      ds->B1.ensure(n);
+      ds->B2.ensure(n);
+      bool need = n > 1 && !(cons->kl1 > 0 && n <= cons->kl1);
+      while (need && ds->bv_ncomp > 1) {
+        ds->scan(metric, ds->B1.p, ds->B2.p, true, INT_UNSET, INT_UNSET, ds->bv_thr_hi, 0,
+                 ds->tile_pairs());
+        int64_t added = ds->bv_finish_round(ds->B1.p, ds->B2.p);
+        if (added == 0) break;
+      }
+      ds->bv_end(cons->kl1, out_merges, out_n_merges, out_assign, out_rounds, out_stop);
+    } else {
+      // ---------------- top-P rounds with exact engine semantics
+      ds->stats.path = NNM_PATH_ROUNDS;
+      const int64_t kl1 = cons->kl1, kl2 = cons->kl2, kl3 = cons->kl3, kl4 = cons->kl4;
+      double thr = INFINITY;
+      if (!std::isnan(cons->dmax)) thr = metric == EUCLIDEAN ? cons->dmax * cons->dmax : cons->dmax;
+      std::vector<int64_t> par(n), sz(n, 1);
+      for (int64_t i = 0; i < n; ++i) par[i] = i;
+      auto find = [&](int64_t x) {
+        int64_t r = x;
+        while (par[r] != r) r = par[r];
+        while (par[x] != r) {
+          int64_t nx = par[x];
+          par[x] = r;
+          x = nx;
+        }
+        return r;
+      };
+      int64_t count = n, nm = 0, rounds = 0;
+      ds->comp.ensure(ds->ld);
+      ds->psize.ensure(ds->ld);
+      ds->rmap.ensure(n);
+      ds->rsize.ensure(n);
+      fill_comp_kernel<<<blocks_for(ds->ld), 256, 0, ds->st>>>(ds->comp.p, ds->psize.p, n, ds->ld); note_launch();
+      iota_kernel<<<blocks_for(n), 256, 0, ds->st>>>(ds->rmap.p, (int)n); note_launch();
+      ones_kernel<<<blocks_for(n), 256, 0, ds->st>>>(ds->rsize.p, (int)n); note_launch();
+      CUDA_TRY(cudaGetLastError());
+      int reason = 0;
+      std::vector<Cand> buf;
+      std::vector<int64_t> order;
+      std::vector<int64_t> snap_size;  // round-start size lookups
+      std::vector<int2> hmap, hsize;
+      for (;;) {
+        if (count == 1) { reason = NNM_STOP_SINGLE_CLUSTER; break; }
+        if (kl1 > 0 && count <= kl1) { reason = NNM_STOP_KL1; break; }
+        ds->top_p(metric, thr, clamp_int(kl2), clamp_int(kl3), P, buf);
+        if (buf.empty()) { reason = NNM_STOP_NO_ELIGIBLE; break; }
+        ++rounds;
+        const int64_t L = (int64_t)buf.size();
+        // order_batch (engine.py:73-87): stable partition by round-start sizes
+        order.resize(L);
+        if (kl4 > 0) {
+          std::vector<char> pri(L);
+          for (int64_t t = 0; t < L; ++t) {
+            int64_t s = std::min(sz[find(buf[t].a)], sz[find(buf[t].b)]);
+            pri[t] = s < kl4;
+          }
+          int64_t k = 0;
+          for (int64_t t = 0; t < L; ++t) if (pri[t]) order[k++] = t;
+          for (int64_t t = 0; t < L; ++t) if (!pri[t]) order[k++] = t;
+        } else {
+          for (int64_t t = 0; t < L; ++t) order[t] = t;
+        }
+        // process_batch (engine.py:90-143)
+        int64_t same = 0, s2 = 0, s3 = 0, unproc = 0, merged = 0;
+        std::vector<int64_t> touched;
+        bool stop = false;
+        for (int64_t pos = 0; pos < L; ++pos) {
+          const Cand& c = buf[order[pos]];
+          int64_t ra = find(c.a), rb = find(c.b);
+          if (ra == rb) { ++same; continue; }
+          int64_t sa = sz[ra], sb = sz[rb];
+          if (kl2 > 0 && (sa > kl2 || sb > kl2)) { ++s2; continue; }
+          if (kl3 > 0 && sa + sb > kl3) { ++s3; continue; }
+          int64_t keep = std::min(ra, rb), drop = std::max(ra, rb);
+          par[drop] = keep;
+          sz[keep] += sz[drop];
+          --count;
+          touched.push_back(drop);
+          touched.push_back(keep);
+          nnm_merge& m = out_merges[nm++];
+          m.round = rounds;
+          m.root_a = keep;
+          m.root_b = drop;
+          m.dist = metric == EUCLIDEAN ? std::sqrt(c.d) : c.d;
+          m.new_size = sz[keep];
+          m.point_a = c.a;
+          m.point_b = c.b;
+          ++merged;
+          if (count == 1 || (kl1 > 0 && count <= kl1)) {
+            unproc = L - pos - 1;
+            stop = true;
+            break;
+          }
+        }
+        if (out_counters && n_counters < counters_cap) {
+          nnm_round_counters& rc = out_counters[n_counters];
+          rc.round = rounds;
+          rc.selected = L;
+          rc.merged = merged;
+          rc.same_root = same;
+          rc.kl2 = s2;
+          rc.kl3 = s3;
+          rc.unprocessed = unproc;
+        }
+        ++n_counters;
+
+        // refresh the device snapshot: root map + root sizes for touched roots
+        hmap.clear();
+        hsize.clear();
+        for (int64_t r : touched) {
+          int64_t f = find(r);
+          hmap.push_back(make_int2((int)r, (int)f));
+          hsize.push_back(make_int2((int)f, (int)std::min<int64_t>(sz[f], INT_UNSET - 1)));
+        }
+        if (!hmap.empty()) {
+          ds->kv.ensure(hmap.size() + hsize.size());
+          CUDA_TRY(cudaMemcpyAsync(ds->kv.p, hmap.data(), hmap.size() * sizeof(int2), cudaMemcpyHostToDevice, ds->st));
+          CUDA_TRY(cudaMemcpyAsync(ds->kv.p + hmap.size(), hsize.data(), hsize.size() * sizeof(int2), cudaMemcpyHostToDevice, ds->st));
+          scatter_kernel<<<blocks_for(hmap.size()), 256, 0, ds->st>>>(ds->kv.p, (int)hmap.size(), ds->rmap.p); note_launch();
+          scatter_kernel<<<blocks_for(hsize.size()), 256, 0, ds->st>>>(ds->kv.p + hmap.size(), (int)hsize.size(), ds->rsize.p); note_launch();
+          snapshot_update_kernel<<<blocks_for(n), 256, 0, ds->st>>>((int)n, ds->comp.p, ds->psize.p, ds->rmap.p, ds->rsize.p); note_launch();
+          CUDA_TRY(cudaGetLastError());
+          ds->sync();  // host vectors are reused next round
+        }
+      }
+      for (int64_t i = 0; i < n; ++i) out_assign[i] = find(i);
+      *out_n_merges = nm;
+      *out_rounds = rounds;
+      *out_stop = reason;
+    }
+    if (out_n_counters) *out_n_counters = n_counters;
+    ds->stats.total_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    ds->stats.kernel_launches = g_launches.load() - launches0;
+    if (stats) *stats = ds->stats;
+  });
+}
+
+// ---- staged Boruvka API (multi-GPU driver) ----------------------------------
+int nnm_bv_begin(nnm_dataset* ds, int32_t metric, double dmax, int64_t* out_tile_pairs) {
+  return guarded([&] {
+    if (!ds) invalid("null dataset");
+    check_metric(metric);
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    ds->stats = nnm_stats{};
+    ds->stats.path = NNM_PATH_BORUVKA;
+    ds->bv_begin(metric, dmax);
+    if (out_tile_pairs) *out_tile_pairs = ds->tile_pairs();
+  });
+}
+
+int nnm_bv_scan(nnm_dataset* ds, int64_t w_begin, int64_t w_end, uint64_t* B1_dev, uint64_t* B2_dev) {
+  return guarded([&] {
+    if (!ds || !B1_dev || !B2_dev) invalid("null argument");
+    if (w_begin < 0 || w_end < w_begin || w_end > ds->tile_pairs()) invalid("bad tile-pair range");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
+    ds->scan(ds->bv_metric, reinterpret_cast<unsigned long long*>(B1_dev),
+             reinterpret_cast<unsigned long long*>(B2_dev), true, INT_UNSET, INT_UNSET,
+             ds->bv_thr_hi, w_begin, w_end);
+    ds->sync();
+  });
+}
+
+}  // extern "C"
+
+namespace nnm {
+__global__ void second_kernel(int n, const unsigned long long* b1l, const unsigned long long* b2l,
+                              const unsigned long long* b1g, unsigned long long* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = (b1l[i] == b1g[i]) ? b2l[i] : b1l[i];
+}
+}  // namespace nnm
+
+extern "C" {
+int nnm_bv_second(nnm_dataset* ds, const uint64_t* B1loc, const uint64_t* B2loc,
+                  const uint64_t* B1glob, uint64_t* B2c) {
+  return guarded([&] {
+    if (!ds) invalid("null dataset");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
+    second_kernel<<<blocks_for(ds->n), 256, 0, ds->st>>>(
+        (int)ds->n, reinterpret_cast<const unsigned long long*>(B1loc),
+        reinterpret_cast<const unsigned long long*>(B2loc),
+        reinterpret_cast<const unsigned long long*>(B1glob),
+        reinterpret_cast<unsigned long long*>(B2c)); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    ds->sync();
+  });
+}
+
+int nnm_bv_finish_round(nnm_dataset* ds, const uint64_t* B1_dev, const uint64_t* B2_dev,
+                        int64_t* out_edges) {
+  return guarded([&] {
+    if (!ds) invalid("null dataset");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
+    *out_edges = ds->bv_finish_round(reinterpret_cast<const unsigned long long*>(B1_dev),
+                                     reinterpret_cast<const unsigned long long*>(B2_dev));
+  });
+}
+
+int nnm_bv_end(nnm_dataset* ds, int64_t kl1, nnm_merge* out_merges, int64_t* out_n_merges,
+               int64_t* out_assign, int64_t* out_rounds, int32_t* out_stop, nnm_stats* stats) {
+  return guarded([&] {
+    if (!ds) invalid("null dataset");
+    if (kl1 == 0) invalid("kl1 must be a positive count, got 0");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    ds->bv_end(kl1, out_merges, out_n_merges, out_assign, out_rounds, out_stop);
+    if (stats) *stats = ds->stats;
+  });
+}
+}  // extern "C"

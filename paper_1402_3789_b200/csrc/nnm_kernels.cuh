@@ -1,0 +1,49 @@
+// nnm_kernels.cuh -- kernel argument blocks and launch wrappers (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nnm_common.cuh"
+
+namespace nnm {
+
+struct ScanArgs {
+  const float* X32;  // [d][ld] SoA, +inf padded
+  int64_t ld;        // n_pad
+  int n, d, T;       // points, dims, tiles (n_pad / TILE)
+  const int* comp;   // [n_pad]
+  const int* psize;  // [n_pad] (SIZES variants)
+  int kl2, kl3;      // INT_UNSET when unset
+  float thr_hi;      // screened dmax bound (INFINITY when unset)
+  int64_t w_begin, w_end;  // linear range of upper-triangular tile pairs
+  unsigned long long* B1;  // [n] best screened key per row
+  unsigned long long* B2;  // [n] second-best (TOP2 only)
+};
+
+struct CollectArgs {
+  const float* XR;  // gathered rows, SoA [d][ldr]
+  int64_t ldr;
+  int nr;
+  const int* rid;   // global index of each gathered row
+  const float* XC;  // columns, SoA [d][ldc]
+  int64_t ldc;
+  int nc;
+  const int* cid;   // global index of each column (nullptr: identity)
+  int d;
+  const int* comp;  // global-indexed
+  const int* psize;
+  int kl2, kl3;
+  const float* rbound;  // per gathered row: collect pairs with screened value <= bound
+  int triangle;         // keep only gi < gj
+  int2* out;
+  unsigned long long* count;
+  unsigned long long cap;
+};
+
+size_t scan_smem_bytes(int d);
+size_t collect_smem_bytes(int d);
+int scan_occupancy(int metric, int d);
+cudaError_t launch_scan(int metric, const ScanArgs& a, bool top2, int grid, cudaStream_t st);
+cudaError_t launch_collect(int metric, const CollectArgs& a, int grid, cudaStream_t st);
+
+}  // namespace nnm

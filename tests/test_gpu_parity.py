@@ -1,0 +1,193 @@
+"""GPU parity: the CUDA path through the C ABI vs the reference's golden vectors
+and the pinned C oracle.  Bit-exact for every key, label and index; merge heights
+are compared bit-exact too (the FP64 keys are scipy-order exact).  All @gpu."""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from nnm_testutil import golden, same_partition
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("root_a", "root_b", "dist", "new_size", "point_a", "point_b")
+
+
+@pytest.fixture(scope="module")
+def nnm():
+    import paper_1402_3789_b200 as pkg
+    from paper_1402_3789_b200 import _native
+
+    _native.load()
+    return pkg
+
+
+def _o(v):
+    v = int(v)
+    return None if v < 0 else v
+
+
+def _records(merges):
+    arr = getattr(merges, "array", None)
+    if arr is not None:
+        return arr
+    return np.array([(e.round, e.root_a, e.root_b, e.dist, e.new_size, e.point_a, e.point_b)
+                     for e in merges], dtype=[("round", np.int64), ("root_a", np.int64),
+                                              ("root_b", np.int64), ("dist", np.float64),
+                                              ("new_size", np.int64), ("point_a", np.int64),
+                                              ("point_b", np.int64)])
+
+
+def test_pairwise_bitwise_vs_scipy_golden(nnm):
+    from paper_1402_3789_b200.metrics import MetricKind, internal_pairwise
+
+    g = golden("metric_tiles.npz")
+    for i in range(int(g["count"])):
+        got = internal_pairwise(MetricKind.parse(str(g[f"metric_{i}"])), g[f"x_{i}"], g[f"y_{i}"])
+        assert np.array_equal(got, g[f"D_{i}"]), i
+
+
+def test_top_p_vs_reference_golden(nnm):
+    from paper_1402_3789_b200.metrics import MetricKind
+    from paper_1402_3789_b200.pairgen import EligibilitySnapshot, gpu_top_p
+
+    g = golden("topp_cases.npz")
+    for i in range(int(g["count"])):
+        kl2, kl3, P = (int(v) for v in g[f"args_{i}"])
+        thr = float(g[f"thr_{i}"])
+        ds = nnm.Dataset(values=g[f"X_{i}"])
+        snap = EligibilitySnapshot(g[f"roots_{i}"], g[f"sizes_{i}"],
+                                   nnm.ConstraintSet(kl2=_o(kl2), kl3=_o(kl3)),
+                                   None if math.isnan(thr) else thr,
+                                   MetricKind.parse(str(g[f"metric_{i}"])))
+        buf = gpu_top_p(ds, snap, P)
+        assert np.array_equal(buf.dist, g[f"dist_{i}"]), i
+        assert np.array_equal(buf.a, g[f"a_{i}"]), i
+        assert np.array_equal(buf.b, g[f"b_{i}"]), i
+
+
+@pytest.mark.parametrize("exact_rounds", [False, True])
+def test_run_vs_reference_engine_golden(nnm, exact_rounds):
+    g = golden("run_cases.npz")
+    for i in range(int(g["count"])):
+        kl1, kl2, kl3, kl4, P = (int(v) for v in g[f"cons_{i}"])
+        dm = float(g[f"dmax_{i}"])
+        cfg = nnm.RunConfig(constraints=nnm.ConstraintSet(kl1=_o(kl1), kl2=_o(kl2), kl3=_o(kl3),
+                                                          kl4=_o(kl4),
+                                                          dmax=None if math.isnan(dm) else dm),
+                            pairs_per_batch=P, metric=nnm.MetricKind.parse(str(g[f"metric_{i}"])),
+                            exact_rounds=exact_rounds)
+        res = nnm.run(nnm.Dataset(values=g[f"X_{i}"]), cfg)
+        got, want = _records(res.merges), g[f"merges_{i}"]
+        assert len(got) == len(want), i
+        for f in FIELDS:
+            assert np.array_equal(got[f], want[f]), (i, f)
+        assert np.array_equal(res.assignments, g[f"assign_{i}"]), i
+        assert res.stop_reason == str(g[f"stop_{i}"]), i
+        if exact_rounds or kl4 >= 0 or kl2 >= 0 or kl3 >= 0:
+            assert np.array_equal(got["round"], want["round"]), i
+            assert res.rounds == int(g[f"rounds_{i}"]), i
+            rc = np.array([[c[k] for k in ("round", "selected", "merged", "same_root", "kl2",
+                                           "kl3", "unprocessed")] for c in res.round_counters],
+                          dtype=np.int64).reshape(-1, 7)
+            assert np.array_equal(rc, g[f"counters_{i}"]), i
+
+
+def test_c1_full_run_vs_reference(nnm):
+    """BASELINE config 1: 10k x 8, 5 blobs, unconstrained, P=256 (reference run here)."""
+    from paper_1402_3789_b200.datagen import config_dataset
+
+    g = golden("c1_run.npz")
+    res = nnm.run(nnm.Dataset(values=config_dataset("c1")), nnm.RunConfig(pairs_per_batch=256))
+    got = _records(res.merges)
+    for f in FIELDS:
+        assert np.array_equal(got[f], g["merges"][f]), f
+    assert np.array_equal(res.assignments, g["assign"])
+    assert res.stop_reason == str(g["stop"])
+
+
+def test_c2_analogue_rounds_vs_reference(nnm):
+    g = golden("c2_small_run.npz")
+    cfg = nnm.RunConfig(constraints=nnm.ConstraintSet(kl1=12, kl2=300, kl3=450, kl4=150),
+                        pairs_per_batch=256)
+    res = nnm.run(nnm.Dataset(values=g["X"]), cfg)
+    got = _records(res.merges)
+    for f in ("round",) + FIELDS:
+        assert np.array_equal(got[f], g["merges"][f]), f
+    assert res.rounds == int(g["rounds"])
+    assert np.array_equal(res.assignments, g["assign"])
+
+
+@pytest.mark.parametrize("metric", ["euclidean", "squared-euclidean", "manhattan", "chebyshev"])
+@pytest.mark.parametrize("kind", ["blobs", "ties", "dups"])
+def test_boruvka_vs_oracle_flat(nnm, metric, kind):
+    from oracle import nnm_oracle as orc
+
+    rng = np.random.default_rng(hash((metric, kind)) % 2**32)
+    n = 1500
+    if kind == "blobs":
+        X = nnm.generate_synthetic(n, 7, 9, 1.0, seed=11)[0]
+    elif kind == "ties":
+        X = rng.integers(-4, 5, size=(n, 3)).astype(np.float64)
+    else:
+        X = np.repeat(rng.normal(size=(n // 3, 5)), 3, axis=0)
+    for cons in ({}, {"dmax": 1.5}, {"kl1": 17}, {"dmax": 0.0}):
+        m_or, a_or = orc.single_linkage(X, metric=metric, **cons)
+        res = nnm.fit(X, metric=metric, **cons)
+        got = _records(res.merges)
+        assert len(got) == len(m_or), cons
+        for f in FIELDS:
+            assert np.array_equal(got[f], m_or[f]), (cons, f)
+        assert np.array_equal(res.assignments, a_or), cons
+
+
+def test_staged_multi_range_equals_single(nnm):
+    """Emulate R ranks on one GPU: disjoint tile-pair ranges + min-combine of keys."""
+    import ctypes
+
+    from paper_1402_3789_b200 import _native
+    from paper_1402_3789_b200.distributed import shard_range
+
+    X = nnm.generate_synthetic(3000, 6, 12, 1.0, seed=3)[0]
+    want = nnm.fit(X)
+    lib = _native.load()
+    dd = _native.DeviceDataset(X)
+    tp = ctypes.c_int64()
+    _native.check(lib.nnm_bv_begin(dd.handle, 0, np.nan, ctypes.byref(tp)))
+    import torch
+
+    n = X.shape[0]
+    R = 3
+    while True:
+        parts = []
+        for r in range(R):
+            lo, hi = shard_range(tp.value, r, R)
+            b1 = torch.empty(n, dtype=torch.int64, device="cuda")
+            b2 = torch.empty(n, dtype=torch.int64, device="cuda")
+            _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
+            parts.append((b1, b2))
+        g1 = torch.stack([p[0] for p in parts]).min(0).values
+        c2 = []
+        for b1, b2 in parts:
+            out = torch.empty_like(b1)
+            _native.check(lib.nnm_bv_second(dd.handle, b1.data_ptr(), b2.data_ptr(), g1.data_ptr(),
+                                            out.data_ptr()))
+            c2.append(out)
+        g2 = torch.stack(c2).min(0).values
+        added = ctypes.c_int64()
+        _native.check(lib.nnm_bv_finish_round(dd.handle, g1.data_ptr(), g2.data_ptr(),
+                                              ctypes.byref(added)))
+        if added.value == 0:
+            break
+    merges = np.zeros(n - 1, dtype=_native.MERGE_DTYPE)
+    assign = np.empty(n, np.int64)
+    nm, rounds = ctypes.c_int64(), ctypes.c_int64()
+    stop = ctypes.c_int32()
+    _native.check(lib.nnm_bv_end(dd.handle, -1, merges.ctypes.data, ctypes.byref(nm),
+                                 assign.ctypes.data, ctypes.byref(rounds), ctypes.byref(stop), None))
+    for f in FIELDS + ("round",):
+        assert np.array_equal(merges[: nm.value][f], want.merges.array[f]), f
+    assert np.array_equal(assign, want.assignments)
