@@ -130,7 +130,7 @@ def cpu_baseline(X, seconds_target: float = 12.0) -> dict:
         orc.top_p(S, roots, sizes, 256, threads=threads)
         return time.perf_counter() - t0
 
-    m = 4000
+    m = 16000  # calibration sample (~1 s), then size the timed sample to ~seconds_target
     t = one(m)
     rate = m * (m - 1) / 2 / t
     m = int(min(X.shape[0], max(4000, (2 * rate * seconds_target) ** 0.5)))

@@ -436,6 +436,44 @@ __global__ void scatter_kernel(const int2* __restrict__ kv, int cnt, int* arr) {
   if (t < cnt) arr[kv[t].x] = kv[t].y;
 }
 
+// effective sizes for the fused kl2 / kl3 rule: size > kl2 -> SIZE_BIG, so that
+// (sa <= kl2 && sb <= kl2 && sa + sb <= kl3)  <=>  eff_a + eff_b <= ksum (pairgen.py:169-187)
+__global__ void eff_size_kernel(const int* __restrict__ psize, int64_t ld, int kl2,
+                                int* __restrict__ eff) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ld) return;
+  int s = psize[i];
+  eff[i] = (kl2 != INT_UNSET && s > kl2) ? SIZE_BIG : s;
+}
+
+// per-tile [min, max] component label of the tile's real points
+__global__ void tile_range_kernel(const int* __restrict__ comp, int64_t n, int T, int2* out) {
+  int t = blockIdx.x;
+  int lo = 0x7FFFFFFF, hi = -0x7FFFFFFF;
+  int64_t i = (int64_t)t * TILE + threadIdx.x;
+  if (i < n) {
+    lo = comp[i];
+    hi = lo;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+  }
+  __shared__ int slo[4], shi[4];
+  if ((threadIdx.x & 31) == 0) {
+    slo[threadIdx.x >> 5] = lo;
+    shi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 4; ++w) {
+      lo = min(lo, slo[w]);
+      hi = max(hi, shi[w]);
+    }
+    out[t] = make_int2(lo, hi);
+  }
+}
+
 __global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -474,7 +512,8 @@ struct nnm_dataset {
   double maxnorm = 0.0;
   DevBuf<unsigned long long> scratch_u64;
 
-  DevBuf<int> comp, psize;
+  DevBuf<int> comp, psize, psize_eff;
+  DevBuf<int2> tile_range;
   DevBuf<unsigned long long> B1, B2;
   // boruvka
   int bv_metric = 0;
@@ -541,11 +580,27 @@ struct nnm_dataset {
 
   int64_t tile_pairs() const { return (int64_t)T * (T + 1) / 2; }
 
+  static int size_rule(int kl2, int kl3) {
+    if (kl3 != INT_UNSET) return kl3;
+    if (kl2 != INT_UNSET) return 2 * kl2;
+    return INT_UNSET;
+  }
+
+  const int* eff_sizes(int kl2) {
+    psize_eff.ensure(ld);
+    eff_size_kernel<<<blocks_for(ld), 256, 0, st>>>(psize.p, ld, kl2, psize_eff.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    return psize_eff.p;
+  }
+
   // full or partial screening scan into (b1, b2); times the launch with events
   void scan(int metric, unsigned long long* b1, unsigned long long* b2, bool top2, int kl2, int kl3,
             float thr_hi, int64_t w_begin, int64_t w_end) {
     fill_none(b1, n);
     if (b2) fill_none(b2, n);
+    tile_range.ensure(T);
+    tile_range_kernel<<<T, TILE, 0, st>>>(comp.p, n, T, tile_range.p); note_launch();
+    const int ksum = size_rule(kl2, kl3);
     ScanArgs a;
     a.X32 = X32.p;
     a.ld = ld;
@@ -553,9 +608,9 @@ struct nnm_dataset {
     a.d = d;
     a.T = T;
     a.comp = comp.p;
-    a.psize = psize.p ? psize.p : comp.p;
-    a.kl2 = kl2;
-    a.kl3 = kl3;
+    a.psize = ksum != INT_UNSET ? eff_sizes(kl2) : comp.p;
+    a.ksum = ksum;
+    a.tile_range = tile_range.p;
     a.thr_hi = thr_hi;
     a.w_begin = w_begin;
     a.w_end = w_end;
@@ -617,9 +672,9 @@ struct nnm_dataset {
       a.cid = cols;
       a.d = d;
       a.comp = comp.p;
-      a.psize = psize.p ? psize.p : comp.p;
-      a.kl2 = kl2;
-      a.kl3 = kl3;
+      const int ksum = size_rule(kl2, kl3);
+      a.psize = ksum != INT_UNSET ? eff_sizes(kl2) : comp.p;
+      a.ksum = ksum;
       a.rbound = bounds;
       a.triangle = triangle;
       a.out = pairs.p;
@@ -895,7 +950,13 @@ void check_constraints(const nnm_constraints* c) {
     invalid("dmax must be nonnegative, got " + std::to_string(c->dmax));
 }
 
-int clamp_int(int64_t v) { return v < 0 ? INT_UNSET : (int)std::min<int64_t>(v, INT_UNSET - 1); }
+// kl2 / kl3 as kernel ints: a cap >= n never binds (two disjoint clusters hold <= n
+// points), so clamp to n; the fused size rule needs n < 2^28 (SIZE_BIG = 2^29).
+int clamp_int(int64_t v, int64_t n) {
+  if (v < 0) return INT_UNSET;
+  if (n >= (int64_t)1 << 28) throw NnmError{NNM_E_UNSUPPORTED, "kl2/kl3 need n < 2^28"};
+  return (int)std::min<int64_t>(v, n);
+}
 
 void init_device(int32_t device, int* sms) {
   int count = 0;
@@ -1038,7 +1099,7 @@ int nnm_top_p(nnm_dataset* ds, int32_t metric, const int64_t* roots, const int64
     CUDA_TRY(cudaMemcpyAsync(ds->comp.p, hc.data(), ds->ld * sizeof(int), cudaMemcpyHostToDevice, ds->st));
     CUDA_TRY(cudaMemcpyAsync(ds->psize.p, hs.data(), ds->ld * sizeof(int), cudaMemcpyHostToDevice, ds->st));
     std::vector<Cand> res;
-    ds->top_p(metric, std::isnan(thr) ? INFINITY : thr, clamp_int(kl2), clamp_int(kl3), P, res);
+    ds->top_p(metric, std::isnan(thr) ? INFINITY : thr, clamp_int(kl2, ds->n), clamp_int(kl3, ds->n), P, res);
     for (size_t t = 0; t < res.size(); ++t) {
       out_dist[t] = res[t].d;
       out_a[t] = res[t].a;
@@ -1115,7 +1176,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       for (;;) {
         if (count == 1) { reason = NNM_STOP_SINGLE_CLUSTER; break; }
         if (kl1 > 0 && count <= kl1) { reason = NNM_STOP_KL1; break; }
-        ds->top_p(metric, thr, clamp_int(kl2), clamp_int(kl3), P, buf);
+        ds->top_p(metric, thr, clamp_int(kl2, ds->n), clamp_int(kl3, ds->n), P, buf);
         if (buf.empty()) { reason = NNM_STOP_NO_ELIGIBLE; break; }
         ++rounds;
         const int64_t L = (int64_t)buf.size();
@@ -1136,7 +1197,6 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
         // process_batch (engine.py:90-143)
         int64_t same = 0, s2 = 0, s3 = 0, unproc = 0, merged = 0;
         std::vector<int64_t> touched;
-        bool stop = false;
         for (int64_t pos = 0; pos < L; ++pos) {
           const Cand& c = buf[order[pos]];
           int64_t ra = find(c.a), rb = find(c.b);
@@ -1161,7 +1221,6 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
           ++merged;
           if (count == 1 || (kl1 > 0 && count <= kl1)) {
             unproc = L - pos - 1;
-            stop = true;
             break;
           }
         }

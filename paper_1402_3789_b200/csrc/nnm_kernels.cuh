@@ -7,13 +7,16 @@
 
 namespace nnm {
 
+constexpr int SIZE_BIG = 1 << 29;  // effective size of clusters above kl2
+
 struct ScanArgs {
   const float* X32;  // [d][ld] SoA, +inf padded
   int64_t ld;        // n_pad
   int n, d, T;       // points, dims, tiles (n_pad / TILE)
   const int* comp;   // [n_pad]
-  const int* psize;  // [n_pad] (SIZES variants)
-  int kl2, kl3;      // INT_UNSET when unset
+  const int* psize;  // [n_pad] effective sizes (> kl2 mapped to SIZE_BIG) (SIZES variants)
+  int ksum;          // eligible iff psize[a] + psize[b] <= ksum (INT_UNSET: no size rule)
+  const int2* tile_range;  // [T] min / max component label of each tile's real points
   float thr_hi;      // screened dmax bound (INFINITY when unset)
   int64_t w_begin, w_end;  // linear range of upper-triangular tile pairs
   unsigned long long* B1;  // [n] best screened key per row
@@ -31,8 +34,8 @@ struct CollectArgs {
   const int* cid;   // global index of each column (nullptr: identity)
   int d;
   const int* comp;  // global-indexed
-  const int* psize;
-  int kl2, kl3;
+  const int* psize;  // effective sizes, see ScanArgs
+  int ksum;
   const float* rbound;  // per gathered row: collect pairs with screened value <= bound
   int triangle;         // keep only gi < gj
   int2* out;

@@ -67,20 +67,27 @@ __device__ __forceinline__ void accumulate(float2& acc, float2 y, float x) {
   }
 }
 
-// 8x8 register tile: rows from sX (local rows row0..row0+7), cols from sY.
+// Warp-local column of a thread's column slot c (0..7): two float4 groups 32
+// columns apart, so the 8 lanes of an LDS.128 phase read 128 contiguous bytes
+// (bank-conflict free).  Within the CTA tile: wc*64 + wcol(tc, c).
+__device__ __forceinline__ int wcol(int tc, int c) { return (c >> 2) * 32 + tc * 4 + (c & 3); }
+
+// 8x8 register tile: rows row0..row0+7 of sX, columns colw + wcol(tc, 0..7) of sY.
 template <int M>
 __device__ __forceinline__ void tile_8x8(const float* __restrict__ sX, const float* __restrict__ sY,
-                                         int d, int row0, int col0, float2 (&acc)[8][4]) {
+                                         int d, int row0, int colw, int tc, float2 (&acc)[8][4]) {
 #pragma unroll
   for (int r = 0; r < 8; ++r)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[r][q] = make_float2(0.f, 0.f);
+  const float* xp = sX + row0;
+  const float* yp = sY + colw + tc * 4;
 #pragma unroll 2
   for (int k = 0; k < d; ++k) {
-    const float4 xa = *reinterpret_cast<const float4*>(sX + k * TILE + row0);
-    const float4 xb = *reinterpret_cast<const float4*>(sX + k * TILE + row0 + 4);
-    const float4 ya = *reinterpret_cast<const float4*>(sY + k * TILE + col0);
-    const float4 yb = *reinterpret_cast<const float4*>(sY + k * TILE + col0 + 4);
+    const float4 xa = *reinterpret_cast<const float4*>(xp + k * TILE);
+    const float4 xb = *reinterpret_cast<const float4*>(xp + k * TILE + 4);
+    const float4 ya = *reinterpret_cast<const float4*>(yp + k * TILE);
+    const float4 yb = *reinterpret_cast<const float4*>(yp + k * TILE + 32);
     const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
     const float2 yc[4] = {make_float2(ya.x, ya.y), make_float2(ya.z, ya.w),
                           make_float2(yb.x, yb.y), make_float2(yb.z, yb.w)};
@@ -95,7 +102,30 @@ __device__ __forceinline__ float acc_at(const float2 (&acc)[8][4], int r, int c)
   return (c & 1) ? acc[r][c >> 1].y : acc[r][c >> 1].x;
 }
 
-// load a 128-point SoA tile [d][128] + comp/size of its points
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// async copy of a 128-point SoA tile [d][128] (+ its comp / size labels)
+__device__ __forceinline__ void async_tile(float* __restrict__ s, int* __restrict__ sc,
+                                           int* __restrict__ ss, const float* __restrict__ X32,
+                                           int64_t ld, int tile, int d, const int* __restrict__ comp,
+                                           const int* __restrict__ psize, bool sizes) {
+  const int nvec = d * (TILE / 4);
+  const float* base = X32 + (int64_t)tile * TILE;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    int k = v >> 5, q = v & 31;
+    cp_async16(s + k * TILE + q * 4, base + (int64_t)k * ld + q * 4);
+  }
+  const int t = threadIdx.x;
+  if (t < 32) cp_async16(sc + t * 4, comp + (int64_t)tile * TILE + t * 4);
+  else if (sizes && t < 64) cp_async16(ss + (t - 32) * 4, psize + (int64_t)tile * TILE + (t - 32) * 4);
+}
+
+// synchronous variant for the collect kernel (gathered sources)
 __device__ __forceinline__ void load_tile(float* __restrict__ s, const float* __restrict__ X32,
                                           int64_t ld, int tile, int d) {
   const int nvec = d * (TILE / 4);
@@ -106,22 +136,37 @@ __device__ __forceinline__ void load_tile(float* __restrict__ s, const float* __
   }
 }
 
+__device__ __forceinline__ void merge2(unsigned long long& a1, unsigned long long& a2,
+                                       unsigned long long b1, unsigned long long b2) {
+  unsigned long long lo = a1 < b1 ? a1 : b1;
+  unsigned long long hi = a1 < b1 ? b1 : a1;
+  unsigned long long m2 = a2 < b2 ? a2 : b2;
+  a1 = lo;
+  a2 = hi < m2 ? hi : m2;
+}
+
 // ----------------------------------------------------------------------------
 // K1: per-row best-2 (or best-1) eligible partner over a range of tile pairs.
+//
+// Persistent CTA over a contiguous run of tile pairs (I <= J, row-major), so the
+// row tile stays in shared memory and its running top-2 lives in shared memory
+// (one owner thread per row, no atomics) until I changes.  Column tiles are
+// double-buffered with cp.async.  Cross-warp partials go through shared memory;
+// only per-tile column results and per-I row results touch global atomics.
 // ----------------------------------------------------------------------------
 template <int M, bool TOP2, bool SIZES, bool THR>
 __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int dT = p.d * TILE;
   float* sX = reinterpret_cast<float*>(smem_raw);
-  float* sY = sX + p.d * TILE;
-  unsigned long long* rowB1 = reinterpret_cast<unsigned long long*>(sY + p.d * TILE);
-  unsigned long long* rowB2 = rowB1 + TILE;
-  unsigned long long* colB1 = rowB2 + TILE;
-  unsigned long long* colB2 = colB1 + TILE;
-  int* sCompR = reinterpret_cast<int*>(colB2 + TILE);
-  int* sCompC = sCompR + TILE;
-  int* sSizeR = sCompC + TILE;
-  int* sSizeC = sSizeR + TILE;
+  float* sY0 = sX + dT;  // two buffers: sY0, sY0 + dT
+  unsigned long long* rowPart = reinterpret_cast<unsigned long long*>(sY0 + 2 * dT);  // [2][128][2]
+  unsigned long long* colPart = rowPart + 2 * TILE * 2;                               // [4][128][2]
+  unsigned long long* rowRun = colPart + 4 * TILE * 2;                                // [128][2]
+  int* sCompR = reinterpret_cast<int*>(rowRun + TILE * 2);
+  int* sSizeR = sCompR + TILE;
+  int* sCompC0 = sSizeR + TILE;  // [2][128]
+  int* sSizeC0 = sCompC0 + 2 * TILE;  // [2][128]
 
   const int64_t total = p.w_end - p.w_begin;
   const int64_t per = (total + gridDim.x - 1) / gridDim.x;
@@ -134,63 +179,56 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
   const int wr = warp >> 1, wc = warp & 1;
   const int tr = lane >> 3, tc = lane & 7;
   const int row0 = wr * 32 + tr * 8;
-  const int col0 = wc * 64 + tc * 8;
-
-  if (tid < TILE) {
-    rowB1[tid] = NONE_KEY;
-    rowB2[tid] = NONE_KEY;
-    colB1[tid] = NONE_KEY;
-    colB2[tid] = NONE_KEY;
-  }
+  const int colw = wc * 64;
 
   int I, J;
   decode_work(w0, p.T, I, J);
-  int curI = -1;
+  async_tile(sX, sCompR, sSizeR, p.X32, p.ld, I, p.d, p.comp, p.psize, SIZES);
+  async_tile(sY0, sCompC0, sSizeC0, p.X32, p.ld, J, p.d, p.comp, p.psize, SIZES);
+  cp_async_commit();
+  if (tid < TILE) {
+    rowRun[2 * tid] = NONE_KEY;
+    rowRun[2 * tid + 1] = NONE_KEY;
+  }
+  cp_async_wait_all();
+  __syncthreads();
 
+  int buf = 0;
   for (int64_t w = w0; w < w1; ++w) {
-    if (I != curI) {
-      if (curI >= 0) {
-        __syncthreads();
-        if (tid < TILE) {
-          int g = curI * TILE + tid;
-          if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, rowB1[tid], rowB2[tid]);
-          rowB1[tid] = NONE_KEY;
-          rowB2[tid] = NONE_KEY;
-        }
-      }
-      __syncthreads();
-      load_tile(sX, p.X32, p.ld, I, p.d);
-      if (tid < TILE) {
-        sCompR[tid] = p.comp[I * TILE + tid];
-        if (SIZES) sSizeR[tid] = p.psize[I * TILE + tid];
-      }
-      curI = I;
+    // ---- prefetch the next column tile into the other buffer
+    int In = I, Jn = J + 1;
+    if (Jn == p.T) {
+      ++In;
+      Jn = In;
     }
-    load_tile(sY, p.X32, p.ld, J, p.d);
-    if (tid < TILE) {
-      sCompC[tid] = p.comp[J * TILE + tid];
-      if (SIZES) sSizeC[tid] = p.psize[J * TILE + tid];
+    const bool has_next = (w + 1 < w1);
+    if (has_next) {
+      async_tile(sY0 + (buf ^ 1) * dT, sCompC0 + (buf ^ 1) * TILE, sSizeC0 + (buf ^ 1) * TILE,
+                 p.X32, p.ld, Jn, p.d, p.comp, p.psize, SIZES);
+      cp_async_commit();
     }
-    __syncthreads();
+    const float* sY = sY0 + buf * dT;
+    const int* sCompC = sCompC0 + buf * TILE;
+    const int* sSizeC = sSizeC0 + buf * TILE;
+    const bool diag = (I == J);
+    // component labels of the two tiles may coincide only if their ranges overlap
+    const int2 rI = __ldg(p.tile_range + I), rJ = __ldg(p.tile_range + J);
+    const bool may_share = diag || !(rI.y < rJ.x || rJ.y < rI.x);
 
     float2 acc[8][4];
-    tile_8x8<M>(sX, sY, p.d, row0, col0, acc);
+    tile_8x8<M>(sX, sY, p.d, row0, colw, tc, acc);
 
-    // ---- eligibility: comp differ, kl2 / kl3 on snapshot sizes, dmax screen
     int cr[8], cc[8], sr[8], sc[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       cr[t] = sCompR[row0 + t];
-      cc[t] = sCompC[col0 + t];
+      cc[t] = sCompC[colw + wcol(tc, t)];
       if (SIZES) {
         sr[t] = sSizeR[row0 + t];
-        sc[t] = sSizeC[col0 + t];
+        sc[t] = sSizeC[colw + wcol(tc, t)];
       }
     }
-    // keys: row side carries the warp-local column (6 bits), col side the
-    // warp-local row (5 bits), packed into the low mantissa bits.
-    uint32_t rk1[8], rk2[8];
-    uint32_t ck1[8], ck2[8];
+    uint32_t rk1[8], rk2[8], ck1[8], ck2[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       rk1[t] = 0xFFFFFFFFu;
@@ -198,20 +236,18 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
       ck1[t] = 0xFFFFFFFFu;
       ck2[t] = 0xFFFFFFFFu;
     }
-    const bool diag = (I == J);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         float v = acc_at(acc, r, c);
-        bool ok = cr[r] != cc[c];
-        if (SIZES) ok = ok && sr[r] <= p.kl2 && sc[c] <= p.kl2 && sr[r] + sc[c] <= p.kl3;
+        bool ok = true;
+        if (may_share) ok = cr[r] != cc[c];
+        if (SIZES) ok = ok && (sr[r] + sc[c] <= p.ksum);
         if (THR) ok = ok && (v <= p.thr_hi);
         uint32_t bits = ok ? __float_as_uint(v) : INF_BITS;
-        uint32_t kr = (bits & ~63u) | (uint32_t)(tc * 8 + c);
-        if (TOP2) {
-          rk2[r] = min(rk2[r], max(rk1[r], kr));
-        }
+        uint32_t kr = (bits & ~63u) | (uint32_t)wcol(tc, c);
+        if (TOP2) rk2[r] = min(rk2[r], max(rk1[r], kr));
         rk1[r] = min(rk1[r], kr);
         if (!diag) {
           uint32_t kc = (bits & ~31u) | (uint32_t)(tr * 8 + r);
@@ -241,14 +277,16 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
           s1 = rk1[r];
           s2 = rk2[r];
         }
-      const unsigned long long jb = (unsigned long long)J * TILE + wc * 64;
+      const unsigned long long jb = (unsigned long long)J * TILE + colw;
       unsigned long long k1 = ((s1 & ~63u) >= INF_BITS)
                                   ? NONE_KEY
                                   : (((unsigned long long)(s1 & ~63u) << 32) | (jb + (s1 & 63u)));
       unsigned long long k2 = NONE_KEY;
       if (TOP2 && (s2 & ~63u) < INF_BITS)
         k2 = ((unsigned long long)(s2 & ~63u) << 32) | (jb + (s2 & 63u));
-      insert_top2(rowB1 + row0 + tc, TOP2 ? rowB2 + row0 + tc : nullptr, k1, k2);
+      unsigned long long* dst = rowPart + (wc * TILE + row0 + tc) * 2;
+      dst[0] = k1;
+      dst[1] = k2;
     }
     // ---- col side: merge across the 4 lanes sharing columns (xor 8,16)
     if (!diag) {
@@ -281,33 +319,58 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
         unsigned long long k2 = NONE_KEY;
         if (TOP2 && (s2 & ~31u) < INF_BITS)
           k2 = ((unsigned long long)(s2 & ~31u) << 32) | (ib + (s2 & 31u));
-        insert_top2(colB1 + col0 + want, TOP2 ? colB2 + col0 + want : nullptr, k1, k2);
+        unsigned long long* dst = colPart + (wr * TILE + colw + wcol(tc, want)) * 2;
+        dst[0] = k1;
+        dst[1] = k2;
       }
     }
-    __syncthreads();
-    if (!diag && tid < TILE) {
-      int g = J * TILE + tid;
-      if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, colB1[tid], colB2[tid]);
-      colB1[tid] = NONE_KEY;
-      colB2[tid] = NONE_KEY;
+    __syncthreads();  // (A) partials complete; sX / sY[buf] no longer read
+    if (tid < TILE) {
+      unsigned long long a1 = rowRun[2 * tid], a2 = rowRun[2 * tid + 1];
+      merge2(a1, a2, rowPart[2 * tid], rowPart[2 * tid + 1]);
+      merge2(a1, a2, rowPart[2 * (TILE + tid)], rowPart[2 * (TILE + tid) + 1]);
+      const bool flush = !has_next || In != I;
+      if (flush) {
+        const int g = I * TILE + tid;
+        if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, a1, a2);
+        a1 = NONE_KEY;
+        a2 = NONE_KEY;
+      }
+      rowRun[2 * tid] = a1;
+      rowRun[2 * tid + 1] = a2;
+    } else if (!diag) {
+      const int c = tid - TILE;
+      unsigned long long a1 = colPart[2 * c], a2 = colPart[2 * c + 1];
+#pragma unroll
+      for (int q = 1; q < 4; ++q) merge2(a1, a2, colPart[2 * (q * TILE + c)], colPart[2 * (q * TILE + c) + 1]);
+      const int g = J * TILE + c;
+      if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, a1, a2);
     }
-    // next work item
-    if (++J == p.T) {
-      ++I;
-      J = I;
+    if (has_next && In != I) {
+      async_tile(sX, sCompR, sSizeR, p.X32, p.ld, In, p.d, p.comp, p.psize, SIZES);
+      cp_async_commit();
     }
-    __syncthreads();
-  }
-  // final row flush
-  if (tid < TILE) {
-    int g = curI * TILE + tid;
-    if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, rowB1[tid], rowB2[tid]);
+    cp_async_wait_all();
+    __syncthreads();  // (B) next tiles resident, row/col partial buffers free
+    I = In;
+    J = Jn;
+    buf ^= 1;
   }
 }
 
 size_t scan_smem_bytes(int d) {
-  return (size_t)2 * d * TILE * sizeof(float) + 4 * TILE * sizeof(unsigned long long) +
-         4 * TILE * sizeof(int);
+  return (size_t)3 * d * TILE * sizeof(float) + (2 + 4 + 1) * TILE * 2 * sizeof(unsigned long long) +
+         6 * TILE * sizeof(int);
+}
+
+int scan_occupancy(int metric, int d) {
+  int blocks = 0;
+  size_t sm = scan_smem_bytes(d);
+  cudaFuncSetAttribute(scan_rows_kernel<EUCLIDEAN, true, false, false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &blocks, scan_rows_kernel<EUCLIDEAN, true, false, false>, SCAN_THREADS, sm);
+  return blocks > 0 ? blocks : 1;
 }
 
 template <int M, bool TOP2, bool SIZES, bool THR>
@@ -322,7 +385,7 @@ static cudaError_t launch_scan_t(const ScanArgs& a, int grid, cudaStream_t st) {
 
 template <int M>
 static cudaError_t launch_scan_m(const ScanArgs& a, bool top2, int grid, cudaStream_t st) {
-  const bool sizes = (a.kl2 != INT_UNSET) || (a.kl3 != INT_UNSET);
+  const bool sizes = a.ksum != INT_UNSET;
   const bool thr = a.thr_hi < INFINITY;
   if (top2) {
     if (sizes) return thr ? launch_scan_t<M, true, true, true>(a, grid, st)
@@ -350,16 +413,6 @@ cudaError_t launch_scan(int metric, const ScanArgs& a, bool top2, int grid, cuda
   }
 }
 
-int scan_occupancy(int metric, int d) {
-  int blocks = 0;
-  size_t sm = scan_smem_bytes(d);
-  cudaFuncSetAttribute(scan_rows_kernel<EUCLIDEAN, true, false, false>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &blocks, scan_rows_kernel<EUCLIDEAN, true, false, false>, SCAN_THREADS, sm);
-  return blocks > 0 ? blocks : 1;
-}
-
 // ----------------------------------------------------------------------------
 // K2: collect every eligible pair whose screened value is <= the row's bound.
 // Rows come from a gathered SoA block (XR, rid); columns from XC (cid or identity).
@@ -382,17 +435,13 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) collect_kernel(CollectArgs p)
   const int wr = warp >> 1, wc = warp & 1;
   const int tr = lane >> 3, tc = lane & 7;
   const int row0 = wr * 32 + tr * 8;
-  const int col0 = wc * 64 + tc * 8;
+  const int colw = wc * 64;
 
   const int rtiles = (p.nr + TILE - 1) / TILE;
   const int ctiles = (p.nc + TILE - 1) / TILE;
   const int64_t items = (int64_t)rtiles * ctiles;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int RT = (int)(it / ctiles), CT = (int)(it % ctiles);
-    if (p.triangle) {
-      // A x A: only tile pairs with RT <= CT carry pairs with gi < gj... not in
-      // general (gathered order is arbitrary), so all tiles are scanned.
-    }
     __syncthreads();
     load_tile(sX, p.XR, p.ldr, RT, p.d);
     load_tile(sY, p.XC, p.ldc, CT, p.d);
@@ -411,7 +460,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) collect_kernel(CollectArgs p)
     }
     __syncthreads();
     float2 acc[8][4];
-    tile_8x8<M>(sX, sY, p.d, row0, col0, acc);
+    tile_8x8<M>(sX, sY, p.d, row0, colw, tc, acc);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int gr = sGR[row0 + r];
@@ -420,11 +469,11 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) collect_kernel(CollectArgs p)
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         float v = acc_at(acc, r, c);
-        const int gc = sGC[col0 + c];
-        bool ok = (v <= bnd) && gr >= 0 && gc >= 0 && cr != sCompC[col0 + c];
+        const int gc = sGC[colw + wcol(tc, c)];
+        bool ok = (v <= bnd) && gr >= 0 && gc >= 0 && cr != sCompC[colw + wcol(tc, c)];
         if (SIZES) {
-          int a = sSizeR[row0 + r], b = sSizeC[col0 + c];
-          ok = ok && a <= p.kl2 && b <= p.kl2 && a + b <= p.kl3;
+          int a = sSizeR[row0 + r], b = sSizeC[colw + wcol(tc, c)];
+          ok = ok && a + b <= p.ksum;
         }
         if (p.triangle) ok = ok && gr < gc;
         if (ok) {
@@ -443,7 +492,7 @@ size_t collect_smem_bytes(int d) {
 template <int M>
 static cudaError_t launch_collect_m(const CollectArgs& a, int grid, cudaStream_t st) {
   size_t sm = collect_smem_bytes(a.d);
-  const bool sizes = (a.kl2 != INT_UNSET) || (a.kl3 != INT_UNSET);
+  const bool sizes = a.ksum != INT_UNSET;
   auto k = sizes ? collect_kernel<M, true> : collect_kernel<M, false>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
