@@ -15,6 +15,7 @@
 // covers 8 x 8 pairs with FADD2/FFMA2 (packed fp32x2) arithmetic.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "nnm_common.cuh"
 #include "nnm_kernels.cuh"
@@ -72,6 +73,18 @@ __device__ __forceinline__ void accumulate(float2& acc, float2 y, float x) {
 // (bank-conflict free).  Within the CTA tile: wc*64 + wcol(tc, c).
 __device__ __forceinline__ int wcol(int tc, int c) { return (c >> 2) * 32 + tc * 4 + (c & 3); }
 
+template <int M>
+__device__ __forceinline__ void fma_step(float2 (&acc)[8][4], float4 xa, float4 xb, float4 ya,
+                                         float4 yb) {
+  const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+  const float2 yc[4] = {make_float2(ya.x, ya.y), make_float2(ya.z, ya.w), make_float2(yb.x, yb.y),
+                        make_float2(yb.z, yb.w)};
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) accumulate<M>(acc[r][q], yc[q], xr[r]);
+}
+
 // 8x8 register tile: rows row0..row0+7 of sX, columns colw + wcol(tc, 0..7) of sY.
 template <int M>
 __device__ __forceinline__ void tile_8x8(const float* __restrict__ sX, const float* __restrict__ sY,
@@ -82,20 +95,28 @@ __device__ __forceinline__ void tile_8x8(const float* __restrict__ sX, const flo
     for (int q = 0; q < 4; ++q) acc[r][q] = make_float2(0.f, 0.f);
   const float* xp = sX + row0;
   const float* yp = sY + colw + tc * 4;
-#pragma unroll 2
-  for (int k = 0; k < d; ++k) {
-    const float4 xa = *reinterpret_cast<const float4*>(xp + k * TILE);
-    const float4 xb = *reinterpret_cast<const float4*>(xp + k * TILE + 4);
-    const float4 ya = *reinterpret_cast<const float4*>(yp + k * TILE);
-    const float4 yb = *reinterpret_cast<const float4*>(yp + k * TILE + 32);
-    const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-    const float2 yc[4] = {make_float2(ya.x, ya.y), make_float2(ya.z, ya.w),
-                          make_float2(yb.x, yb.y), make_float2(yb.z, yb.w)};
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) accumulate<M>(acc[r][q], yc[q], xr[r]);
+  // software-pipelined with two register sets (no copies: IMAD.MOV would run on
+  // the FMA pipe): operands of k+1 load while k computes, hiding LDS latency
+  // behind 64 FMA-pipe instructions even at 2 compute warps per SMSP.
+  float4 a0 = *reinterpret_cast<const float4*>(xp), a1 = *reinterpret_cast<const float4*>(xp + 4);
+  float4 a2 = *reinterpret_cast<const float4*>(yp), a3 = *reinterpret_cast<const float4*>(yp + 32);
+  int k = 0;
+#pragma unroll 1
+  for (; k + 1 < d; k += 2) {
+    const int o1 = (k + 1) * TILE;
+    const float4 b0 = *reinterpret_cast<const float4*>(xp + o1);
+    const float4 b1 = *reinterpret_cast<const float4*>(xp + o1 + 4);
+    const float4 b2 = *reinterpret_cast<const float4*>(yp + o1);
+    const float4 b3 = *reinterpret_cast<const float4*>(yp + o1 + 32);
+    fma_step<M>(acc, a0, a1, a2, a3);
+    const int o2 = min(k + 2, d - 1) * TILE;
+    a0 = *reinterpret_cast<const float4*>(xp + o2);
+    a1 = *reinterpret_cast<const float4*>(xp + o2 + 4);
+    a2 = *reinterpret_cast<const float4*>(yp + o2);
+    a3 = *reinterpret_cast<const float4*>(yp + o2 + 32);
+    fma_step<M>(acc, b0, b1, b2, b3);
   }
+  if (k < d) fma_step<M>(acc, a0, a1, a2, a3);
 }
 
 __device__ __forceinline__ float acc_at(const float2 (&acc)[8][4], int r, int c) {
@@ -363,7 +384,21 @@ size_t scan_smem_bytes(int d) {
          6 * TILE * sizeof(int);
 }
 
+static int g_ws_mode = -1;  // -1: auto, 0: force classic, 1: force warp-specialised
+
+bool scan_use_ws(int d) {
+  if (g_ws_mode < 0) {  // NNM_SCAN_KERNEL=classic|ws (A/B switch for profiling)
+    const char* e = getenv("NNM_SCAN_KERNEL");
+    g_ws_mode = (e && e[0] == 'c') ? 0 : 2;
+  }
+  if (g_ws_mode == 0) return false;
+  return scan_ws_smem_bytes(d) <= 200 * 1024;
+}
+
+void scan_set_mode(int mode) { g_ws_mode = mode; }
+
 int scan_occupancy(int metric, int d) {
+  if (scan_use_ws(d)) return 1;
   int blocks = 0;
   size_t sm = scan_smem_bytes(d);
   cudaFuncSetAttribute(scan_rows_kernel<EUCLIDEAN, true, false, false>,
@@ -373,8 +408,313 @@ int scan_occupancy(int metric, int d) {
   return blocks > 0 ? blocks : 1;
 }
 
+
+// ----------------------------------------------------------------------------
+// K1-WS: warp-specialised variant of K1 (the default for d <= WS_MAX_D).
+//
+// 8 compute warps stream 128x128 distance tiles (FADD2/FFMA2, 8x8 per thread)
+// into a double-buffered, XOR-swizzled shared tile; 4 epilogue warps consume
+// it concurrently: thread t owns row t and column t of the tile, applies the
+// eligibility rule and keeps the top-2 keys.  Producer / consumer hand-off uses
+// named barriers (FULL[b], EMPTY[b]), so the selection work (integer pipe)
+// overlaps the distance math (FMA pipe) instead of following it.
+// Swizzle: element (r, c) lives at r*128 + ((c/4 ^ (r & 31)) * 4) + c%4, which
+// makes the compute warps' STS.128, the row readers' LDS.128 and the column
+// readers' scalar LDS all bank-conflict free.
+// ----------------------------------------------------------------------------
+constexpr int WS_COMPUTE_THREADS = 256;
+constexpr int WS_EPI_THREADS = 256;  // 128 row owners + 128 column owners
+constexpr int WS_THREADS = WS_COMPUTE_THREADS + WS_EPI_THREADS;
+
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ int swz(int r, int q) { return r * TILE + ((q ^ (r & 31)) << 2); }
+
+// running top-2 of u32 keys, two new keys at a time (5 integer min/max ops)
+__device__ __forceinline__ void top2_pair(uint32_t& m1, uint32_t& m2, uint32_t a, uint32_t b) {
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  m2 = umin3(max(m1, lo), m2, hi);
+  m1 = min(m1, lo);
+}
+
+__device__ __forceinline__ unsigned long long widen(uint32_t k, unsigned long long base) {
+  return ((k & ~63u) >= INF_BITS) ? NONE_KEY
+                                  : (((unsigned long long)(k & ~63u) << 32) | (base + (k & 63u)));
+}
+
+template <int M, bool TOP2, bool SIZES, bool THR>
+__global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int dT = p.d * TILE;
+  float* sD = reinterpret_cast<float*>(smem_raw);  // [2][128*128]
+  float* sX0 = sD + 2 * TILE * TILE;               // [2][d*128]
+  float* sY0 = sX0 + 2 * dT;                       // [2][d*128]
+  int* sCR = reinterpret_cast<int*>(sY0 + 2 * dT);  // [2][128] row comps (epilogue)
+  int* sCC = sCR + 2 * TILE;                        // [2][128] col comps
+  int* sSR = sCC + 2 * TILE;                        // [2][128] row eff sizes
+  int* sSC = sSR + 2 * TILE;                        // [2][128] col eff sizes
+
+  const int64_t total = p.w_end - p.w_begin;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = p.w_begin + (int64_t)blockIdx.x * per;
+  const int64_t w1 = min(w0 + per, p.w_end);
+  if (w0 >= w1) return;
+  const int tid = threadIdx.x;
+  int I, J;
+  decode_work(w0, p.T, I, J);
+
+  if (tid < WS_COMPUTE_THREADS) {
+    // =========================== compute warps ===========================
+    const int warp = tid >> 5, lane = tid & 31;
+    const int wr = warp >> 1, wc = warp & 1;
+    const int tr = lane >> 3, tc = lane & 7;
+    const int row0 = wr * 32 + tr * 8;
+    const int colw = wc * 64;
+    // prologue loads (compute threads only; blockDim for the copy loops is 256)
+    {
+      const int nvec = p.d * (TILE / 4);
+      for (int v = tid; v < nvec; v += WS_COMPUTE_THREADS) {
+        int k = v >> 5, q = v & 31;
+        cp_async16(sX0 + k * TILE + q * 4, p.X32 + (int64_t)k * p.ld + (int64_t)I * TILE + q * 4);
+        cp_async16(sY0 + k * TILE + q * 4, p.X32 + (int64_t)k * p.ld + (int64_t)J * TILE + q * 4);
+      }
+      cp_async_commit();
+    }
+    int xb = 0;
+    for (int64_t w = w0; w < w1; ++w) {
+      const int buf = (int)((w - w0) & 1);
+      int In = I, Jn = J + 1;
+      if (Jn == p.T) {
+        ++In;
+        Jn = In;
+      }
+      cp_async_wait_all();
+      bar_sync(1, WS_COMPUTE_THREADS);  // tiles for w resident; everyone done with w-1
+      if (w + 1 < w1) {
+        const int nvec = p.d * (TILE / 4);
+        float* ny = sY0 + (buf ^ 1) * dT;
+        float* nx = sX0 + (xb ^ 1) * dT;
+        const bool newI = In != I;
+        for (int v = tid; v < nvec; v += WS_COMPUTE_THREADS) {
+          int k = v >> 5, q = v & 31;
+          cp_async16(ny + k * TILE + q * 4, p.X32 + (int64_t)k * p.ld + (int64_t)Jn * TILE + q * 4);
+          if (newI)
+            cp_async16(nx + k * TILE + q * 4, p.X32 + (int64_t)k * p.ld + (int64_t)In * TILE + q * 4);
+        }
+        cp_async_commit();
+      }
+      float2 acc[8][4];
+      tile_8x8<M>(sX0 + xb * dT, sY0 + buf * dT, p.d, row0, colw, tc, acc);
+      bar_sync(4 + buf, WS_THREADS);  // EMPTY[buf]
+      float* D = sD + buf * TILE * TILE;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int R = row0 + r;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int q = wc * 16 + h * 8 + tc;
+          float4 v = make_float4(acc[r][2 * h].x, acc[r][2 * h].y, acc[r][2 * h + 1].x,
+                                 acc[r][2 * h + 1].y);
+          *reinterpret_cast<float4*>(D + swz(R, q)) = v;
+        }
+      }
+      bar_arrive(2 + buf, WS_THREADS);  // FULL[buf]
+      if (In != I) xb ^= 1;
+      I = In;
+      J = Jn;
+    }
+    // balance the epilogue's two outstanding EMPTY arrivals
+    bar_sync(4, WS_THREADS);
+    bar_sync(5, WS_THREADS);
+  } else {
+    // =========================== epilogue warps ==========================
+    const int e_id = tid - WS_COMPUTE_THREADS;  // 0..255
+    const bool is_row = e_id < TILE;             // warps 8-11: rows, 12-15: columns
+    const int t = is_row ? e_id : e_id - TILE;   // owned row (or column) of the tile
+    unsigned long long run1 = NONE_KEY, run2 = NONE_KEY;  // row t running top-2 over J
+    bar_arrive(4, WS_THREADS);  // both distance buffers start empty
+    bar_arrive(5, WS_THREADS);
+    for (int64_t w = w0; w < w1; ++w) {
+      const int buf = (int)((w - w0) & 1);
+      int In = I, Jn = J + 1;
+      if (Jn == p.T) {
+        ++In;
+        Jn = In;
+      }
+      const bool diag = (I == J);
+      const int2 rI = __ldg(p.tile_range + I), rJ = __ldg(p.tile_range + J);
+      const bool may_share = diag || !(rI.y < rJ.x || rJ.y < rI.x);
+      int* cr = sCR + buf * TILE;
+      int* cc = sCC + buf * TILE;
+      int* sr = sSR + buf * TILE;
+      int* sc = sSC + buf * TILE;
+      // my own label / size, and publish it for the other role
+      const int mytile = is_row ? I : J;
+      const int myC = __ldg(p.comp + (int64_t)mytile * TILE + t);
+      int myS = 0;
+      (is_row ? cr : cc)[t] = myC;
+      if (SIZES) {
+        myS = __ldg(p.psize + (int64_t)mytile * TILE + t);
+        (is_row ? sr : sc)[t] = myS;
+      }
+      // global second-best (best for top-1) d-parts: stale values are larger,
+      // hence still safe filter thresholds
+      uint32_t growG = 0xFFFFFFFFu, gcolG = 0xFFFFFFFFu;
+      {
+        const unsigned long long* G = TOP2 ? p.B2 : p.B1;
+        const int g = (is_row ? I : J) * TILE + t;
+        if (g < p.n) {
+          const uint32_t v = (uint32_t)(*((volatile const unsigned long long*)(G + g)) >> 32);
+          if (is_row) growG = v;
+          else gcolG = v;
+        }
+      }
+      bar_sync(6, WS_EPI_THREADS);
+      bar_sync(2 + buf, WS_THREADS);  // FULL[buf]
+      const float* D = sD + buf * TILE * TILE;
+      unsigned long long k1 = NONE_KEY, k2 = NONE_KEY;
+      // Filter: a value whose masked d-part exceeds the d-part of a key already
+      // known to survive (running / global second-best; best for top-1) cannot
+      // enter the final top-2, so whole 4-value chunks are skipped with one
+      // warp vote.  Skipped values would only have produced larger keys.
+      if (is_row) {
+        const int tt = t & 31;
+        const float* Drow = D + t * TILE;
+        uint32_t gthr = (uint32_t)((TOP2 ? run2 : run1) >> 32);
+        gthr = min(gthr, growG);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+          uint32_t thr = gthr | 63u;
+#pragma unroll
+          for (int qq = 0; qq < 16; ++qq) {
+            // logical chunk q (compile-time) sits at position q ^ tt: distinct
+            // positions across the warp keep the LDS.128 bank-conflict free
+            const int q = h * 16 + qq;
+            const float4 v4 = *reinterpret_cast<const float4*>(Drow + ((q ^ tt) << 2));
+            const uint32_t b0 = __float_as_uint(v4.x), b1 = __float_as_uint(v4.y);
+            const uint32_t b2 = __float_as_uint(v4.z), b3 = __float_as_uint(v4.w);
+            const uint32_t mn = min(umin3(b0, b1, b2), b3);
+            if (__any_sync(0xFFFFFFFFu, mn <= thr)) {
+              const uint32_t bb[4] = {b0, b1, b2, b3};
+              int4 c4 = make_int4(0, 0, 0, 0), s4 = make_int4(0, 0, 0, 0);
+              if (may_share) c4 = *reinterpret_cast<const int4*>(cc + q * 4);
+              if (SIZES) s4 = *reinterpret_cast<const int4*>(sc + q * 4);
+              const int ca[4] = {c4.x, c4.y, c4.z, c4.w};
+              const int sa[4] = {s4.x, s4.y, s4.z, s4.w};
+              const uint32_t cb = (uint32_t)((q & 15) * 4);
+              uint32_t kk[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                bool ok = true;
+                if (may_share) ok = ca[e] != myC;
+                if (SIZES) ok = ok && (myS + sa[e] <= p.ksum);
+                if (THR) ok = ok && (__uint_as_float(bb[e]) <= p.thr_hi);
+                const uint32_t bits = ok ? bb[e] : INF_BITS;
+                kk[e] = (bits & ~63u) | (cb + e);
+              }
+              if (TOP2) {
+                top2_pair(m1, m2, kk[0], kk[1]);
+                top2_pair(m1, m2, kk[2], kk[3]);
+                thr = min(gthr, m2 & ~63u) | 63u;
+              } else {
+                m1 = min(min(m1, kk[0]), min(min(kk[1], kk[2]), kk[3]));
+                thr = min(gthr, m1 & ~63u) | 63u;
+              }
+            }
+          }
+          const unsigned long long base = (unsigned long long)J * TILE + h * 64;
+          merge2(run1, run2, widen(m1, base), TOP2 ? widen(m2, base) : NONE_KEY);
+          gthr = min(gthr, (uint32_t)((TOP2 ? run2 : run1) >> 32));
+        }
+      } else if (!diag) {
+        // ---- column t: element (r, t) sits at r*128 + (t ^ ((r & 31) << 2))
+        int off[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) off[u] = t ^ (u << 2);
+        uint32_t gthr = gcolG;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
+          uint32_t thr = gthr | 63u;
+#pragma unroll
+          for (int r4 = h * 16; r4 < h * 16 + 16; ++r4) {
+            uint32_t bb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int r = r4 * 4 + u;
+              bb[u] = __float_as_uint(D[r * TILE + off[r & 31]]);
+            }
+            const uint32_t mn = min(umin3(bb[0], bb[1], bb[2]), bb[3]);
+            if (__any_sync(0xFFFFFFFFu, mn <= thr)) {
+              int4 c4 = make_int4(0, 0, 0, 0), s4 = make_int4(0, 0, 0, 0);
+              if (may_share) c4 = *reinterpret_cast<const int4*>(cr + r4 * 4);
+              if (SIZES) s4 = *reinterpret_cast<const int4*>(sr + r4 * 4);
+              const int ca[4] = {c4.x, c4.y, c4.z, c4.w};
+              const int sa[4] = {s4.x, s4.y, s4.z, s4.w};
+              uint32_t kk[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int r = r4 * 4 + u;
+                bool ok = true;
+                if (may_share) ok = ca[u] != myC;
+                if (SIZES) ok = ok && (myS + sa[u] <= p.ksum);
+                if (THR) ok = ok && (__uint_as_float(bb[u]) <= p.thr_hi);
+                const uint32_t bits = ok ? bb[u] : INF_BITS;
+                kk[u] = (bits & ~63u) | (uint32_t)(r & 63);
+              }
+              if (TOP2) {
+                top2_pair(m1, m2, kk[0], kk[1]);
+                top2_pair(m1, m2, kk[2], kk[3]);
+                thr = min(gthr, m2 & ~63u) | 63u;
+              } else {
+                m1 = min(min(m1, kk[0]), min(min(kk[1], kk[2]), kk[3]));
+                thr = min(gthr, m1 & ~63u) | 63u;
+              }
+            }
+          }
+          const unsigned long long base = (unsigned long long)I * TILE + h * 64;
+          merge2(k1, k2, widen(m1, base), TOP2 ? widen(m2, base) : NONE_KEY);
+          gthr = min(gthr, (uint32_t)((TOP2 ? k2 : k1) >> 32));
+        }
+      }
+      bar_arrive(4 + buf, WS_THREADS);  // EMPTY[buf]: distances consumed
+      if (is_row) {
+        if (w + 1 >= w1 || In != I) {
+          const int g = I * TILE + t;
+          if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, run1, run2);
+          run1 = NONE_KEY;
+          run2 = NONE_KEY;
+        }
+      } else if (!diag) {
+        const int g = J * TILE + t;
+        if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, k1, k2);
+      }
+      I = In;
+      J = Jn;
+    }
+  }
+}
+
+size_t scan_ws_smem_bytes(int d) {
+  return (size_t)2 * TILE * TILE * sizeof(float) + (size_t)4 * d * TILE * sizeof(float) +
+         8 * TILE * sizeof(int);
+}
+
 template <int M, bool TOP2, bool SIZES, bool THR>
 static cudaError_t launch_scan_t(const ScanArgs& a, int grid, cudaStream_t st) {
+  if (scan_use_ws(a.d)) {
+    size_t sm = scan_ws_smem_bytes(a.d);
+    auto k = scan_ws_kernel<M, TOP2, SIZES, THR>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k<<<grid, WS_THREADS, sm, st>>>(a);
+    return cudaGetLastError();
+  }
   size_t sm = scan_smem_bytes(a.d);
   auto k = scan_rows_kernel<M, TOP2, SIZES, THR>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
