@@ -93,30 +93,41 @@ __device__ __forceinline__ void tile_8x8(const float* __restrict__ sX, const flo
   for (int r = 0; r < 8; ++r)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[r][q] = make_float2(0.f, 0.f);
-  const float* xp = sX + row0;
-  const float* yp = sY + colw + tc * 4;
+  const float* __restrict__ xp = sX + row0;
+  const float* __restrict__ yp = sY + colw + tc * 4;
   // software-pipelined with two register sets (no copies: IMAD.MOV would run on
   // the FMA pipe): operands of k+1 load while k computes, hiding LDS latency
   // behind 64 FMA-pipe instructions even at 2 compute warps per SMSP.
+  // Pointers advance by TILE floats per k (integer adds on the ALU pipe; IMAD
+  // address math would take FMA-pipe cycles from FFMA2/FADD2).
   float4 a0 = *reinterpret_cast<const float4*>(xp), a1 = *reinterpret_cast<const float4*>(xp + 4);
   float4 a2 = *reinterpret_cast<const float4*>(yp), a3 = *reinterpret_cast<const float4*>(yp + 32);
   int k = 0;
 #pragma unroll 1
-  for (; k + 1 < d; k += 2) {
-    const int o1 = (k + 1) * TILE;
-    const float4 b0 = *reinterpret_cast<const float4*>(xp + o1);
-    const float4 b1 = *reinterpret_cast<const float4*>(xp + o1 + 4);
-    const float4 b2 = *reinterpret_cast<const float4*>(yp + o1);
-    const float4 b3 = *reinterpret_cast<const float4*>(yp + o1 + 32);
+  for (; k + 2 < d; k += 2) {
+    const float4 b0 = *reinterpret_cast<const float4*>(xp + TILE);
+    const float4 b1 = *reinterpret_cast<const float4*>(xp + TILE + 4);
+    const float4 b2 = *reinterpret_cast<const float4*>(yp + TILE);
+    const float4 b3 = *reinterpret_cast<const float4*>(yp + TILE + 32);
     fma_step<M>(acc, a0, a1, a2, a3);
-    const int o2 = min(k + 2, d - 1) * TILE;
-    a0 = *reinterpret_cast<const float4*>(xp + o2);
-    a1 = *reinterpret_cast<const float4*>(xp + o2 + 4);
-    a2 = *reinterpret_cast<const float4*>(yp + o2);
-    a3 = *reinterpret_cast<const float4*>(yp + o2 + 32);
+    xp += 2 * TILE;
+    yp += 2 * TILE;
+    a0 = *reinterpret_cast<const float4*>(xp);
+    a1 = *reinterpret_cast<const float4*>(xp + 4);
+    a2 = *reinterpret_cast<const float4*>(yp);
+    a3 = *reinterpret_cast<const float4*>(yp + 32);
     fma_step<M>(acc, b0, b1, b2, b3);
   }
-  if (k < d) fma_step<M>(acc, a0, a1, a2, a3);
+  if (k + 1 < d) {  // two k left: a holds k, load k+1
+    const float4 b0 = *reinterpret_cast<const float4*>(xp + TILE);
+    const float4 b1 = *reinterpret_cast<const float4*>(xp + TILE + 4);
+    const float4 b2 = *reinterpret_cast<const float4*>(yp + TILE);
+    const float4 b3 = *reinterpret_cast<const float4*>(yp + TILE + 32);
+    fma_step<M>(acc, a0, a1, a2, a3);
+    fma_step<M>(acc, b0, b1, b2, b3);
+  } else {
+    fma_step<M>(acc, a0, a1, a2, a3);
+  }
 }
 
 __device__ __forceinline__ float acc_at(const float2 (&acc)[8][4], int r, int c) {
@@ -495,31 +506,38 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
       cp_async_wait_all();
       bar_sync(1, WS_COMPUTE_THREADS);  // tiles for w resident; everyone done with w-1
       if (w + 1 < w1) {
-        const int nvec = p.d * (TILE / 4);
-        float* ny = sY0 + (buf ^ 1) * dT;
-        float* nx = sX0 + (xb ^ 1) * dT;
+        // this thread copies 16-byte column chunk (tid & 31) of rows k = tid/32 + 8i
+        float* ny = sY0 + (buf ^ 1) * dT + (tid >> 5) * TILE + (tid & 31) * 4;
+        float* nx = sX0 + (xb ^ 1) * dT + (tid >> 5) * TILE + (tid & 31) * 4;
+        const float* gy = p.X32 + (int64_t)(tid >> 5) * p.ld + (int64_t)Jn * TILE + (tid & 31) * 4;
+        const float* gx = p.X32 + (int64_t)(tid >> 5) * p.ld + (int64_t)In * TILE + (tid & 31) * 4;
+        const int64_t gstep = 8 * p.ld;
         const bool newI = In != I;
-        for (int v = tid; v < nvec; v += WS_COMPUTE_THREADS) {
-          int k = v >> 5, q = v & 31;
-          cp_async16(ny + k * TILE + q * 4, p.X32 + (int64_t)k * p.ld + (int64_t)Jn * TILE + q * 4);
-          if (newI)
-            cp_async16(nx + k * TILE + q * 4, p.X32 + (int64_t)k * p.ld + (int64_t)In * TILE + q * 4);
+        for (int k = tid >> 5; k < p.d; k += 8) {
+          cp_async16(ny, gy);
+          if (newI) cp_async16(nx, gx);
+          ny += 8 * TILE;
+          nx += 8 * TILE;
+          gy += gstep;
+          gx += gstep;
         }
         cp_async_commit();
       }
       float2 acc[8][4];
       tile_8x8<M>(sX0 + xb * dT, sY0 + buf * dT, p.d, row0, colw, tc, acc);
       bar_sync(4 + buf, WS_THREADS);  // EMPTY[buf]
-      float* D = sD + buf * TILE * TILE;
+      // element (R, 4q..4q+3) -> R*128 + ((q ^ (R & 31)) << 2); with R = row0 + r and
+      // q = (wc*2 + h)*8 + tc the XOR splits into ((wc*2+h) ^ tr) << 5 | (tc ^ r) << 2
+      float* D = sD + buf * TILE * TILE + row0 * TILE;
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const int R = row0 + r;
+        const int lo = (tc ^ r) << 2;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int q = wc * 16 + h * 8 + tc;
+          const int off = r * TILE + ((((wc << 1) | h) ^ tr) << 5 | lo);
           float4 v = make_float4(acc[r][2 * h].x, acc[r][2 * h].y, acc[r][2 * h + 1].x,
                                  acc[r][2 * h + 1].y);
-          *reinterpret_cast<float4*>(D + swz(R, q)) = v;
+          *reinterpret_cast<float4*>(D + off) = v;
         }
       }
       bar_arrive(2 + buf, WS_THREADS);  // FULL[buf]
