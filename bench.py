@@ -281,14 +281,15 @@ def run_gpu(args) -> None:
     peak = ctypes.c_double()
     _native.check(lib.nnm_measure_fp32_peak(local, ctypes.byref(peak)))
     avg_launch_ms = scan_ms / max(scans, 1)
-    # algorithmic flops of one full-range scan launch (per rank: its share of tile pairs)
-    flops_launch = (sum(s["pairs_evaluated"] for s in stats) / max(scans, 1)) * 3 * d
-    achieved = flops_launch / (avg_launch_ms / 1e3) / 1e12
+    # algorithmic flops (3d per evaluated pair: d sub, d mul, d add) over the CUDA-event
+    # time of all scan launches (launch sizes differ once tile pairs are pruned)
+    pairs_eval = sum(s["pairs_evaluated"] for s in stats)
+    achieved = pairs_eval * 3 * d / (scan_ms / 1e3) / 1e12
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value if peak.value else None, "traffic": _load_traffic(),
                 "kernel": "scan_rows_kernel (fused FP32 distance + eligibility + per-row top-2)",
                 "peak_source": "measured FFMA2 microbenchmark on this GPU (MEASURED_PEAKS.json has no FP32 entry)",
-                "avg_launch_ms": avg_launch_ms,
+                "avg_launch_ms": avg_launch_ms, "launches": scans,
                 "scan_share_of_step": scan_ms / (ms_dev * args.steps)}
     if rank != 0:
         if dist is not None:
@@ -298,6 +299,8 @@ def run_gpu(args) -> None:
     cfg = {"workload": desc, "n": n, "d": d, "metric": "euclidean", "pairs_per_step": pairs_step,
            "l2": "inputs larger than L2 (X32 %.0f MB + X64 %.0f MB > 126 MB)" % (n * d * 4 / 1e6, X.nbytes / 1e6),
            "seconds_to_dendrogram": ms_dev / 1e3, "boruvka_rounds": stats[-1]["boruvka_rounds"],
+           "pairs_covered_per_s": sum(s["pairs_covered"] for s in stats) / (ms_dev * args.steps / 1e3),
+           "pairs_evaluated_fraction": pairs_eval / max(1.0, sum(s["pairs_covered"] for s in stats)),
            "merges": n - 1, "parallelism": f"tile-pair shards x{world}" if world > 1 else "1 GPU"}
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,

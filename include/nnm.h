@@ -85,6 +85,7 @@ typedef struct {
   int64_t exact_evals;     /* FP64 pair evaluations */
   int64_t boruvka_rounds;
   int64_t kernel_launches; /* libnnm kernels launched by the call (library sorts excluded) */
+  double pairs_covered;    /* pairs the rounds decided (evaluated or excluded by an exact bound) */
 } nnm_stats;
 
 int nnm_abi_version(void);

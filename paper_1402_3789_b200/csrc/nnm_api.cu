@@ -17,6 +17,8 @@
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
 #include <thrust/sort.h>
+#include <thrust/scan.h>
+#include <thrust/unique.h>
 
 #include <algorithm>
 #include <atomic>
@@ -297,6 +299,14 @@ __global__ void fix_rows_kernel(const int* __restrict__ rows, int nr,
   if (rb_d[rows[t]] == NONE_KEY) rb_j[rows[t]] = -1;
 }
 
+struct ItemLess {  // order int2 {I, J} stored as u64 (low = I, high = J) by (I, J)
+  __host__ __device__ bool operator()(unsigned long long a, unsigned long long b) const {
+    const long long ia = (int)(a & 0xFFFFFFFFull), ib = (int)(b & 0xFFFFFFFFull);
+    if (ia != ib) return ia < ib;
+    return (int)(a >> 32) < (int)(b >> 32);
+  }
+};
+
 struct Edge {
   double d;
   int a, b;
@@ -356,6 +366,250 @@ __global__ void relabel_kernel(int n, int* comp, const int* __restrict__ parent)
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   comp[i] = parent[comp[i]];
+}
+
+
+// ---- exact tile-pair pruning (Boruvka) -------------------------------------
+// Tile geometry: FP64 centre (mean of the tile's real points) and radius (max
+// metric distance of a point to the centre, inflated).  For any i in I, j in J:
+//   dist(i, j) >= dist(c_I, c_J) - R_I - R_J   (triangle inequality)
+// so LB_IJ bounds the exact scipy value of every pair of the tile pair.
+template <int M>
+__device__ __forceinline__ double metric_dist_real(const double* a, const double* b, int d) {
+  double acc = 0.0;
+  for (int k = 0; k < d; ++k) {
+    double t = fabs(a[k] - b[k]);
+    if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc += t * t;
+    else if (M == MANHATTAN) acc += t;
+    else acc = fmax(acc, t);
+  }
+  return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? sqrt(acc) : acc;
+}
+
+template <int M>
+__global__ void tile_geom_kernel(const double* __restrict__ X64, int64_t n, int d,
+                                 double* __restrict__ centers, double* __restrict__ radius) {
+  const int T0 = blockIdx.x;
+  const int64_t base = (int64_t)T0 * TILE;
+  const int m = (int)((n - base) < TILE ? (n - base) : TILE);
+  extern __shared__ double sc[];  // [d]
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += X64[(base + i) * d + k];
+    sc[k] = s / m;
+    centers[(int64_t)T0 * d + k] = sc[k];
+  }
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < m) r = metric_dist_real<M>(X64 + (base + threadIdx.x) * d, sc, d);
+  for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xFFFFFFFFu, r, o));
+  __shared__ double sr[4];
+  if ((threadIdx.x & 31) == 0) sr[threadIdx.x >> 5] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    r = fmax(fmax(sr[0], sr[1]), fmax(sr[2], sr[3]));
+    radius[T0] = r * (1.0 + 1e-9) + 1e-300;
+  }
+}
+
+// lower bound on the exact internal value of every pair of tile pair (I, J)
+template <int M>
+__device__ __forceinline__ double tile_lb(const double* __restrict__ centers,
+                                          const double* __restrict__ radius, int d, int I, int J) {
+  if (I == J) return 0.0;
+  double dc = metric_dist_real<M>(centers + (int64_t)I * d, centers + (int64_t)J * d, d);
+  double r = dc * (1.0 - 1e-9) - radius[I] - radius[J];
+  if (!(r > 0.0)) return 0.0;
+  return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? r * r * (1.0 - 1e-9) : r * (1.0 - 1e-9);
+}
+
+__device__ __forceinline__ bool same_single(const int2* __restrict__ tr, int I, int J) {
+  const int2 a = tr[I], b = tr[J];
+  return a.x == a.y && b.x == b.y && a.x == b.x;
+}
+
+// Phase 1: for each tile I the PK tile pairs with the smallest LB among tiles
+// that can hold a cross-component pair with I (every pair of I x J in one
+// component is useless).  Seeds the component upper bounds.
+constexpr int PK = 8;
+template <int M>
+__global__ void phase1_kernel(const double* __restrict__ centers, const double* __restrict__ radius,
+                              const int2* __restrict__ trange, int T, int d, int2* __restrict__ out) {
+  const int I = blockIdx.x;
+  double bl[2] = {INFINITY, INFINITY};
+  int bj[2] = {-1, -1};
+  for (int J = threadIdx.x; J < T; J += blockDim.x) {
+    if (same_single(trange, I, J)) continue;
+    double lb = tile_lb<M>(centers, radius, d, I, J);
+    if (lb < bl[1] || (lb == bl[1] && J < bj[1])) {
+      if (lb < bl[0] || (lb == bl[0] && J < bj[0])) {
+        bl[1] = bl[0]; bj[1] = bj[0]; bl[0] = lb; bj[0] = J;
+      } else {
+        bl[1] = lb; bj[1] = J;
+      }
+    }
+  }
+  __shared__ double sl[512];
+  __shared__ int sj[512];
+  sl[2 * threadIdx.x] = bl[0]; sj[2 * threadIdx.x] = bj[0];
+  sl[2 * threadIdx.x + 1] = bl[1]; sj[2 * threadIdx.x + 1] = bj[1];
+  __syncthreads();
+  // PK rounds of block arg-min over the 512 candidates (tiny)
+  __shared__ double rl[8];
+  __shared__ int ri[8];
+  for (int k = 0; k < PK; ++k) {
+    double v = INFINITY;
+    int at = -1;
+    for (int c = threadIdx.x; c < 2 * blockDim.x; c += blockDim.x) {
+      if (sj[c] >= 0 && (sl[c] < v || (sl[c] == v && (at < 0 || sj[c] < sj[at])))) {
+        v = sl[c];
+        at = c;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      int oa = __shfl_xor_sync(0xFFFFFFFFu, at, o);
+      if (oa >= 0 && (at < 0 || ov < v || (ov == v && sj[oa] < sj[at]))) {
+        v = ov;
+        at = oa;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      rl[threadIdx.x >> 5] = v;
+      ri[threadIdx.x >> 5] = at;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bv = INFINITY;
+      int ba = -1;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (ri[w] >= 0 && (ba < 0 || rl[w] < bv || (rl[w] == bv && sj[ri[w]] < sj[ba]))) {
+          bv = rl[w];
+          ba = ri[w];
+        }
+      int2 it = make_int2(-1, -1);
+      if (ba >= 0) {
+        int J = sj[ba];
+        it = make_int2(min(I, J), max(I, J));
+        sj[ba] = -1;  // remove
+      }
+      out[(int64_t)I * PK + k] = it;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int64_t tri_index(int T, int I, int J) {
+  return (int64_t)I * T - (int64_t)I * (I - 1) / 2 + (J - I);
+}
+
+__global__ void mark_items_kernel(const int2* __restrict__ items, int64_t cnt, int T,
+                                  unsigned* __restrict__ bits) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  int64_t w = tri_index(T, items[t].x, items[t].y);
+  atomicOr(bits + (w >> 5), 1u << (w & 31));
+}
+
+// component upper bound: exact value of each row's screened-best partner
+template <int M>
+__global__ void ucomp_kernel(const double* __restrict__ X64, int n, int d,
+                             const unsigned long long* __restrict__ B1, const int* __restrict__ comp,
+                             double thr, unsigned long long* U) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long k = B1[i];
+  if (!key_valid(k)) return;
+  int j = (int)key_index(k);
+  double e = exact_dist<M>(X64 + (int64_t)i * d, X64 + (int64_t)j * d, d);
+  if (e <= thr) atomicMin(U + comp[i], dbits(e));
+}
+
+__global__ void tile_umax_kernel(const int* __restrict__ comp, int64_t n,
+                                 const unsigned long long* __restrict__ U, double thr,
+                                 double* __restrict__ umax) {
+  const int T0 = blockIdx.x;
+  int64_t i = (int64_t)T0 * TILE + threadIdx.x;
+  double v = -INFINITY;
+  if (i < n) {
+    unsigned long long u = U[comp[i]];
+    v = (u == NONE_KEY) ? thr : fmin(bitsd(u), thr);
+  }
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  __shared__ double s[4];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) umax[T0] = fmax(fmax(s[0], s[1]), fmax(s[2], s[3]));
+}
+
+// Phase 2 enumeration, pass 1: keep flags + per-row-tile counts.
+template <int M>
+__global__ void enum_count_kernel(const double* __restrict__ centers, const double* __restrict__ radius,
+                                  const int2* __restrict__ trange, const double* __restrict__ umax,
+                                  const unsigned* __restrict__ bits, int T, int d,
+                                  unsigned char* __restrict__ keep, int* __restrict__ counts) {
+  const int I = blockIdx.x;
+  const double uI = umax[I];
+  int c = 0;
+  const int64_t w0 = tri_index(T, I, I);
+  for (int J = I + threadIdx.x; J < T; J += blockDim.x) {
+    const int64_t w = w0 + (J - I);
+    bool k = !((bits[w >> 5] >> (w & 31)) & 1u) && !same_single(trange, I, J);
+    if (k) k = tile_lb<M>(centers, radius, d, I, J) <= fmax(uI, umax[J]);
+    keep[w] = k;
+    c += k;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  __shared__ int s[8];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    counts[I] = t;
+  }
+}
+
+// pass 2: ordered compaction (items sorted by I, then J)
+__global__ void enum_write_kernel(const unsigned char* __restrict__ keep,
+                                  const long long* __restrict__ offsets, int T,
+                                  int2* __restrict__ items) {
+  const int I = blockIdx.x;
+  const int64_t w0 = tri_index(T, I, I);
+  long long base = offsets[I];
+  __shared__ int warp_tot[8];
+  for (int J0 = I; J0 < T; J0 += blockDim.x) {
+    const int J = J0 + threadIdx.x;
+    const int k = (J < T) ? keep[w0 + (J - I)] : 0;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, k);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int before = __popc(m & ((1u << lane) - 1));
+    if (lane == 0) warp_tot[wid] = __popc(m);
+    __syncthreads();
+    int off = 0, tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      if (w < wid) off += warp_tot[w];
+      tot += warp_tot[w];
+    }
+    if (k) items[base + off + before] = make_int2(I, J);
+    base += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt, int64_t n,
+                                  unsigned long long* acc) {
+  // real point pairs covered by a list of tile pairs (for the stats)
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (t < cnt) {
+    int2 it = items[t];
+    long long mI = n - (int64_t)it.x * TILE; if (mI > TILE) mI = TILE;
+    long long mJ = n - (int64_t)it.y * TILE; if (mJ > TILE) mJ = TILE;
+    v = (it.x == it.y) ? (unsigned long long)(mI * (mI - 1) / 2) : (unsigned long long)(mI * mJ);
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(acc, v);
 }
 
 // ---- round path -----------------------------------------------------------
@@ -532,6 +786,17 @@ struct nnm_dataset {
   DevBuf<int2> pairs;
   DevBuf<double> pair_d;
   DevBuf<int> flag;
+  // pruning
+  int geom_metric = -1;
+  DevBuf<double> tcenter, tradius, tumax;
+  DevBuf<int2> items1, items2;
+  DevBuf<unsigned> pbits;
+  DevBuf<unsigned char> pkeep;
+  DevBuf<int> pcount;
+  DevBuf<long long> poffset;
+  DevBuf<unsigned long long> ucomp;
+  double pairs_covered = 0.0;
+  const int2* p1_list = nullptr;
   // round path
   DevBuf<Cand> cands, cands2;
   DevBuf<int> active, rmap, rsize;
@@ -595,9 +860,12 @@ struct nnm_dataset {
 
   // full or partial screening scan into (b1, b2); times the launch with events
   void scan(int metric, unsigned long long* b1, unsigned long long* b2, bool top2, int kl2, int kl3,
-            float thr_hi, int64_t w_begin, int64_t w_end) {
-    fill_none(b1, n);
-    if (b2) fill_none(b2, n);
+            float thr_hi, int64_t w_begin, int64_t w_end, const int2* items = nullptr,
+            bool reset = true) {
+    if (reset) {
+      fill_none(b1, n);
+      if (b2) fill_none(b2, n);
+    }
     tile_range.ensure(T);
     tile_range_kernel<<<T, TILE, 0, st>>>(comp.p, n, T, tile_range.p); note_launch();
     const int ksum = size_rule(kl2, kl3);
@@ -614,11 +882,12 @@ struct nnm_dataset {
     a.thr_hi = thr_hi;
     a.w_begin = w_begin;
     a.w_end = w_end;
+    a.items = items;
     a.B1 = b1;
     a.B2 = b2;
     int occ = scan_occupancy(metric, d);
-    int64_t items = w_end - w_begin;
-    int grid = (int)std::min<int64_t>(items, (int64_t)sms * occ);
+    int64_t nitems = w_end - w_begin;
+    int grid = (int)std::min<int64_t>(nitems, (int64_t)sms * occ);
     if (grid < 1) return;
     CUDA_TRY(cudaEventRecord(ev0, st));
     CUDA_TRY(launch_scan(metric, a, top2, grid, st));
@@ -629,8 +898,14 @@ struct nnm_dataset {
     CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
     stats.scan_ms += ms;
     stats.scans += 1;
-    // unordered real pairs covered by this work range
-    stats.pairs_evaluated += (double)n * (double)(n - 1) / 2.0 * ((double)items / (double)tile_pairs());
+    if (items) {  // exact count of real pairs in the listed tile pairs
+      counters.ensure(8);
+      CUDA_TRY(cudaMemsetAsync(counters.p + 7, 0, sizeof(unsigned long long), st));
+      item_pairs_kernel<<<blocks_for(w_end - w_begin), 256, 0, st>>>(items + w_begin, w_end - w_begin, n, counters.p + 7); note_launch();
+      stats.pairs_evaluated += (double)read1(counters.p + 7);
+    } else {  // unordered real pairs covered by this range of the triangle
+      stats.pairs_evaluated += (double)n * (double)(n - 1) / 2.0 * ((double)(w_end - w_begin) / (double)tile_pairs());
+    }
   }
 
   // collect pairs (row list x columns) with screened value <= per-row bound
@@ -737,6 +1012,98 @@ struct nnm_dataset {
     CUDA_TRY(cudaMemsetAsync(counters.p, 0, 8 * sizeof(unsigned long long), st));
     bv_round = 0;
     bv_ncomp = n;
+  }
+
+  void ensure_geometry(int metric) {
+    int kind = (metric == SQEUCLIDEAN) ? EUCLIDEAN : metric;
+    if (geom_metric == kind) return;
+    tcenter.ensure((size_t)T * d);
+    tradius.ensure(T);
+    size_t sm = (size_t)d * sizeof(double);
+    switch (kind) {
+      case MANHATTAN: tile_geom_kernel<MANHATTAN><<<T, TILE, sm, st>>>(X64.p, n, d, tcenter.p, tradius.p); break;
+      case CHEBYSHEV: tile_geom_kernel<CHEBYSHEV><<<T, TILE, sm, st>>>(X64.p, n, d, tcenter.p, tradius.p); break;
+      default: tile_geom_kernel<EUCLIDEAN><<<T, TILE, sm, st>>>(X64.p, n, d, tcenter.p, tradius.p);
+    }
+    note_launch();
+    CUDA_TRY(cudaGetLastError());
+    geom_metric = kind;
+  }
+
+  template <int M>
+  void pruned_lists(int64_t& n1, int64_t& n2) {
+    const int64_t W = tile_pairs();
+    // phase-1 seeds: PK nearest cross-capable tiles per tile
+    items1.ensure((size_t)T * PK);
+    phase1_kernel<M><<<T, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, T, d, items1.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    auto* k64 = reinterpret_cast<unsigned long long*>(items1.p);  // (I, J) -> J << 32 | I order
+    // sort by (I, J): int2 memory is {x=I, y=J}; as u64 little-endian = J << 32 | I -> swap to key
+    thrust::sort(thrust::cuda::par.on(st), k64, k64 + (size_t)T * PK, ItemLess());
+    auto* end = thrust::unique(thrust::cuda::par.on(st), k64, k64 + (size_t)T * PK);
+    n1 = end - k64;
+    // drop the (-1,-1) padding, which sorts first
+    int2 first = read1(items1.p);
+    int64_t skip = (first.x < 0) ? 1 : 0;
+    n1 -= skip;
+    int2* list1 = items1.p + skip;
+    pbits.ensure((size_t)(W + 31) / 32);
+    CUDA_TRY(cudaMemsetAsync(pbits.p, 0, ((W + 31) / 32) * sizeof(unsigned), st));
+    if (n1 > 0) { mark_items_kernel<<<blocks_for(n1), 256, 0, st>>>(list1, n1, T, pbits.p); note_launch(); }
+    p1_list = list1;
+    (void)W;
+    n2 = 0;
+  }
+
+  template <int M>
+  void pruned_phase2(int64_t& n2) {
+    const int64_t W = tile_pairs();
+    tumax.ensure(T);
+    tile_umax_kernel<<<T, TILE, 0, st>>>(comp.p, n, ucomp.p, bv_thr, tumax.p); note_launch();
+    pkeep.ensure(W);
+    pcount.ensure(T);
+    poffset.ensure(T + 1);
+    enum_count_kernel<M><<<T, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, tumax.p, pbits.p, T, d,
+                                             pkeep.p, pcount.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    thrust::exclusive_scan(thrust::cuda::par.on(st), pcount.p, pcount.p + T, poffset.p, 0LL);
+    long long last_off = read1(poffset.p + (T - 1));
+    int last_cnt = read1(pcount.p + (T - 1));
+    n2 = last_off + last_cnt;
+    items2.ensure(std::max<int64_t>(n2, 1));
+    if (n2 > 0) { enum_write_kernel<<<T, 256, 0, st>>>(pkeep.p, poffset.p, T, items2.p); note_launch(); }
+    CUDA_TRY(cudaGetLastError());
+  }
+
+  template <int M>
+  void ucomp_t(const unsigned long long* b1) {
+    ucomp_kernel<M><<<blocks_for(n), 256, 0, st>>>(X64.p, (int)n, d, b1, comp.p, bv_thr, ucomp.p); note_launch();
+  }
+
+  // One pruned Boruvka scan: exact per-row keys for every row that can hold its
+  // component's minimum edge.
+  void pruned_scan(int metric) {
+    ensure_geometry(metric);
+    tile_range.ensure(T);
+    tile_range_kernel<<<T, TILE, 0, st>>>(comp.p, n, T, tile_range.p); note_launch();
+    int64_t n1 = 0, n2 = 0;
+    switch (metric) {
+      case MANHATTAN: pruned_lists<MANHATTAN>(n1, n2); break;
+      case CHEBYSHEV: pruned_lists<CHEBYSHEV>(n1, n2); break;
+      default: pruned_lists<EUCLIDEAN>(n1, n2);
+    }
+    fill_none(B1.p, n);
+    fill_none(B2.p, n);
+    if (n1 > 0) scan(metric, B1.p, B2.p, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
+    ucomp.ensure(n);
+    fill_none(ucomp.p, n);
+    switch (metric) {
+      case MANHATTAN: ucomp_t<MANHATTAN>(B1.p); pruned_phase2<MANHATTAN>(n2); break;
+      case CHEBYSHEV: ucomp_t<CHEBYSHEV>(B1.p); pruned_phase2<CHEBYSHEV>(n2); break;
+      default: ucomp_t<EUCLIDEAN>(B1.p); pruned_phase2<EUCLIDEAN>(n2);
+    }
+    if (n2 > 0) scan(metric, B1.p, B2.p, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n2, items2.p, false);
+    pairs_covered += (double)n * (double)(n - 1) / 2.0;
   }
 
   template <int M>
@@ -1123,6 +1490,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
     auto t0 = std::chrono::steady_clock::now();
     const int64_t launches0 = g_launches.load();
     ds->stats = nnm_stats{};
+    ds->pairs_covered = 0.0;
     ds->stats.device = ds->device;
     const int64_t n = ds->n;
     const bool rounds_path = (flags & NNM_FLAG_ROUNDS) || cons->kl2 > 0 || cons->kl3 > 0 || cons->kl4 > 0;
@@ -1134,9 +1502,16 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       ds->B1.ensure(n);
       ds->B2.ensure(n);
       bool need = n > 1 && !(cons->kl1 > 0 && n <= cons->kl1);
+      const char* pe = getenv("NNM_PRUNE");
+      const bool prune = !(pe && pe[0] == '0');
       while (need && ds->bv_ncomp > 1) {
-        ds->scan(metric, ds->B1.p, ds->B2.p, true, INT_UNSET, INT_UNSET, ds->bv_thr_hi, 0,
-                 ds->tile_pairs());
+        if (prune) {
+          ds->pruned_scan(metric);
+        } else {
+          ds->scan(metric, ds->B1.p, ds->B2.p, true, INT_UNSET, INT_UNSET, ds->bv_thr_hi, 0,
+                   ds->tile_pairs());
+          ds->pairs_covered += (double)n * (double)(n - 1) / 2.0;
+        }
         int64_t added = ds->bv_finish_round(ds->B1.p, ds->B2.p);
         if (added == 0) break;
       }
@@ -1264,6 +1639,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
     ds->stats.total_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     ds->stats.kernel_launches = g_launches.load() - launches0;
+    ds->stats.pairs_covered = ds->pairs_covered;
     if (stats) *stats = ds->stats;
   });
 }

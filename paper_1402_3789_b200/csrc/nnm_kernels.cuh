@@ -18,7 +18,8 @@ struct ScanArgs {
   int ksum;          // eligible iff psize[a] + psize[b] <= ksum (INT_UNSET: no size rule)
   const int2* tile_range;  // [T] min / max component label of each tile's real points
   float thr_hi;      // screened dmax bound (INFINITY when unset)
-  int64_t w_begin, w_end;  // linear range of upper-triangular tile pairs
+  int64_t w_begin, w_end;  // range of work items
+  const int2* items;       // nullptr: item w = w-th upper-triangular tile pair; else items[w]
   unsigned long long* B1;  // [n] best screened key per row
   unsigned long long* B2;  // [n] second-best (TOP2 only)
 };

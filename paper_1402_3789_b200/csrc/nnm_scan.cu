@@ -55,6 +55,34 @@ __device__ __forceinline__ void decode_work(int64_t w, int T, int& I, int& J) {
   J = i + (int)(w - start(i));
 }
 
+// Work item w -> tile pair (I, J): either the row-major upper triangle or an
+// explicit list (pruned scans), in both cases sorted by I so row tiles are reused.
+__device__ __forceinline__ void first_item(const ScanArgs& p, int64_t w, int& I, int& J) {
+  if (p.items) {
+    const int2 it = __ldg(p.items + w);
+    I = it.x;
+    J = it.y;
+  } else {
+    decode_work(w, p.T, I, J);
+  }
+}
+
+__device__ __forceinline__ void next_item(const ScanArgs& p, int64_t w, int I, int J, int& In,
+                                          int& Jn) {
+  if (p.items) {
+    const int2 it = (w + 1 < p.w_end) ? __ldg(p.items + w + 1) : make_int2(I, J);
+    In = it.x;
+    Jn = it.y;
+  } else {
+    In = I;
+    Jn = J + 1;
+    if (Jn == p.T) {
+      ++In;
+      Jn = In;
+    }
+  }
+}
+
 template <int M>
 __device__ __forceinline__ void accumulate(float2& acc, float2 y, float x) {
   float2 dd = __fadd2_rn(y, make_float2(-x, -x));
@@ -214,7 +242,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
   const int colw = wc * 64;
 
   int I, J;
-  decode_work(w0, p.T, I, J);
+  first_item(p, w0, I, J);
   async_tile(sX, sCompR, sSizeR, p.X32, p.ld, I, p.d, p.comp, p.psize, SIZES);
   async_tile(sY0, sCompC0, sSizeC0, p.X32, p.ld, J, p.d, p.comp, p.psize, SIZES);
   cp_async_commit();
@@ -228,11 +256,8 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
   int buf = 0;
   for (int64_t w = w0; w < w1; ++w) {
     // ---- prefetch the next column tile into the other buffer
-    int In = I, Jn = J + 1;
-    if (Jn == p.T) {
-      ++In;
-      Jn = In;
-    }
+    int In, Jn;
+    next_item(p, w, I, J, In, Jn);
     const bool has_next = (w + 1 < w1);
     if (has_next) {
       async_tile(sY0 + (buf ^ 1) * dT, sCompC0 + (buf ^ 1) * TILE, sSizeC0 + (buf ^ 1) * TILE,
@@ -476,7 +501,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
   if (w0 >= w1) return;
   const int tid = threadIdx.x;
   int I, J;
-  decode_work(w0, p.T, I, J);
+  first_item(p, w0, I, J);
 
   if (tid < WS_COMPUTE_THREADS) {
     // =========================== compute warps ===========================
@@ -498,11 +523,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
     int xb = 0;
     for (int64_t w = w0; w < w1; ++w) {
       const int buf = (int)((w - w0) & 1);
-      int In = I, Jn = J + 1;
-      if (Jn == p.T) {
-        ++In;
-        Jn = In;
-      }
+      int In, Jn;
+      next_item(p, w, I, J, In, Jn);
       cp_async_wait_all();
       bar_sync(1, WS_COMPUTE_THREADS);  // tiles for w resident; everyone done with w-1
       if (w + 1 < w1) {
@@ -558,11 +580,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
     bar_arrive(5, WS_THREADS);
     for (int64_t w = w0; w < w1; ++w) {
       const int buf = (int)((w - w0) & 1);
-      int In = I, Jn = J + 1;
-      if (Jn == p.T) {
-        ++In;
-        Jn = In;
-      }
+      int In, Jn;
+      next_item(p, w, I, J, In, Jn);
       const bool diag = (I == J);
       const int2 rI = __ldg(p.tile_range + I), rJ = __ldg(p.tile_range + J);
       const bool may_share = diag || !(rI.y < rJ.x || rJ.y < rI.x);
