@@ -130,9 +130,11 @@ int nnm_pairwise(int32_t metric, const double *x, int64_t nx, const double *y, i
  * One process per GPU; every rank holds the full dataset.  Per round each rank
  * scans its share of the upper-triangular tile pairs into (B1, B2), the driver
  * combines the per-row keys across ranks with two all-reduce(min) calls, and
- * every rank then finishes the round identically.  Device buffers are
- * caller-owned (e.g. torch tensors) of n uint64 each. */
-int nnm_bv_begin(nnm_dataset *ds, int32_t metric, double dmax, int64_t *out_tile_pairs);
+ * every rank then finishes the round identically.  Rows live in the library's
+ * spatially ordered, tile-padded view: device key buffers are caller-owned
+ * (e.g. torch tensors) of *out_rows uint64 each. */
+int nnm_bv_begin(nnm_dataset *ds, int32_t metric, double dmax, int64_t *out_tile_pairs,
+                 int64_t *out_rows);
 int nnm_bv_scan(nnm_dataset *ds, int64_t w_begin, int64_t w_end, uint64_t *B1_dev,
                 uint64_t *B2_dev);
 /* B2 contribution for the global second-best: B2c[i] = (B1loc[i] == B1glob[i]) ? B2loc[i] : B1loc[i] */

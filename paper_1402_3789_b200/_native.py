@@ -101,7 +101,7 @@ def load():
         lib.nnm_run.argtypes = [vp, i32, P(Constraints), i64, i32, vp, P(i64), vp, P(i64), P(i32),
                                 vp, i64, P(i64), P(Stats)]
         lib.nnm_pairwise.argtypes = [i32, vp, i64, vp, i64, i32, i32, vp]
-        lib.nnm_bv_begin.argtypes = [vp, i32, dbl, P(i64)]
+        lib.nnm_bv_begin.argtypes = [vp, i32, dbl, P(i64), P(i64)]
         lib.nnm_bv_scan.argtypes = [vp, i64, i64, vp, vp]
         lib.nnm_bv_second.argtypes = [vp, vp, vp, vp, vp]
         lib.nnm_bv_finish_round.argtypes = [vp, vp, vp, P(i64)]

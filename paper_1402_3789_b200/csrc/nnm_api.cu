@@ -21,6 +21,7 @@
 #include <thrust/unique.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -130,6 +131,16 @@ __global__ void prepare_kernel(const double* __restrict__ X64, int64_t n, int d,
   }
 }
 
+// permuted view: X32 SoA of positions (pads +inf)
+__global__ void prepare_view_kernel(const double* __restrict__ X64p, const int* __restrict__ porig,
+                                    int64_t np, int d, float* __restrict__ X32p) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const bool real = porig[p] >= 0;
+  for (int k = 0; k < d; ++k)
+    X32p[(int64_t)k * np + p] = real ? __double2float_rn(X64p[p * d + k]) : INFINITY;
+}
+
 // per-point norm in the metric's norm, rounded up; global max via atomicMax on bits
 __global__ void norms_kernel(const double* __restrict__ X64, int64_t n, int d, int metric,
                              double* __restrict__ norm, unsigned long long* maxbits) {
@@ -186,7 +197,8 @@ __global__ void refine_kernel(const double* __restrict__ X64, int n, int d,
                               const unsigned long long* __restrict__ B2,
                               const double* __restrict__ norm, double maxnorm, ErrModel em,
                               double thr, unsigned long long* rb_d, int* rb_j, double* rowlow,
-                              int* amb, unsigned long long* amb_count) {
+                              int* amb, unsigned long long* amb_count,
+                              const int* __restrict__ orig) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   unsigned long long k1 = B1[i];
@@ -204,7 +216,7 @@ __global__ void refine_kernel(const double* __restrict__ X64, int n, int d,
   double low2 = key_valid(k2) ? exact_lower(em, (double)key_value(k2), R) : INFINITY;
   if (e <= thr) {
     rb_d[i] = dbits(e);
-    rb_j[i] = j;
+    rb_j[i] = orig[j];  // partner as ORIGINAL index (tie-break order of the reference)
     if (low2 > e) return;  // certified: every other partner is strictly farther
   } else {
     rb_d[i] = NONE_KEY;
@@ -228,13 +240,14 @@ __global__ void compmin_ab_kernel(int n, const int* __restrict__ comp,
                                   const unsigned long long* __restrict__ rb_d,
                                   const int* __restrict__ rb_j,
                                   const unsigned long long* __restrict__ cmin_d,
-                                  unsigned long long* cmin_ab) {
+                                  unsigned long long* cmin_ab, const int* __restrict__ orig) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   unsigned long long v = rb_d[i];
   int c = comp[i];
   if (v == NONE_KEY || v != cmin_d[c]) return;
-  unsigned a = (unsigned)min(i, rb_j[i]), b = (unsigned)max(i, rb_j[i]);
+  const int oi = orig[i];  // pair key in original indices: (dist, a, b), model.py:100-106
+  unsigned a = (unsigned)min(oi, rb_j[i]), b = (unsigned)max(oi, rb_j[i]);
   atomicMin(cmin_ab + c, ((unsigned long long)a << 32) | b);
 }
 
@@ -285,11 +298,11 @@ __global__ void rowmin_d_kernel(const int2* __restrict__ pairs, const double* __
 
 __global__ void rowmin_j_kernel(const int2* __restrict__ pairs, const double* __restrict__ dv,
                                 int64_t count, double thr, const unsigned long long* rb_d,
-                                int* rb_j) {
+                                int* rb_j, const int* __restrict__ orig) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
   int2 p = pairs[t];
-  if (dv[t] <= thr && dbits(dv[t]) == rb_d[p.x]) atomicMin(rb_j + p.x, p.y);
+  if (dv[t] <= thr && dbits(dv[t]) == rb_d[p.x]) atomicMin(rb_j + p.x, orig[p.y]);
 }
 
 __global__ void fix_rows_kernel(const int* __restrict__ rows, int nr,
@@ -325,7 +338,8 @@ struct EdgeLess {
 __global__ void hook_kernel(int n, const int* __restrict__ comp,
                             const unsigned long long* __restrict__ cmin_d,
                             const unsigned long long* __restrict__ cmin_ab, int* parent,
-                            Edge* edges, unsigned long long* edge_count, int round) {
+                            Edge* edges, unsigned long long* edge_count, int round,
+                            const int* __restrict__ pos) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n || comp[c] != c) return;
   unsigned long long e = cmin_ab[c];
@@ -334,7 +348,7 @@ __global__ void hook_kernel(int n, const int* __restrict__ comp,
     return;
   }
   int a = (int)(e >> 32), b = (int)(e & 0xFFFFFFFFull);
-  int ca = comp[a], cb = comp[b];
+  int ca = comp[pos[a]], cb = comp[pos[b]];  // a, b are original indices
   int other = (ca == c) ? cb : ca;
   bool mutual = (cmin_ab[other] == e);
   bool record = !mutual || c < other;
@@ -364,7 +378,7 @@ __global__ void jump_kernel(int n, const int* __restrict__ comp, int* parent, in
 
 __global__ void relabel_kernel(int n, int* comp, const int* __restrict__ parent) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || comp[i] < 0) return;
   comp[i] = parent[comp[i]];
 }
 
@@ -387,21 +401,23 @@ __device__ __forceinline__ double metric_dist_real(const double* a, const double
 }
 
 template <int M>
-__global__ void tile_geom_kernel(const double* __restrict__ X64, int64_t n, int d,
+__global__ void tile_geom_kernel(const double* __restrict__ X64, const int* __restrict__ tcount, int d,
                                  double* __restrict__ centers, double* __restrict__ radius) {
+  // real points of a tile are its first tcount[T0] positions (pads follow)
   const int T0 = blockIdx.x;
   const int64_t base = (int64_t)T0 * TILE;
-  const int m = (int)((n - base) < TILE ? (n - base) : TILE);
+  const int m = tcount[T0];
   extern __shared__ double sc[];  // [d]
   for (int k = threadIdx.x; k < d; k += blockDim.x) {
     double s = 0.0;
     for (int i = 0; i < m; ++i) s += X64[(base + i) * d + k];
-    sc[k] = s / m;
+    sc[k] = m > 0 ? s / m : 0.0;
     centers[(int64_t)T0 * d + k] = sc[k];
   }
   __syncthreads();
   double r = 0.0;
   if (threadIdx.x < m) r = metric_dist_real<M>(X64 + (base + threadIdx.x) * d, sc, d);
+  if (m == 0) r = 0.0;
   for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xFFFFFFFFu, r, o));
   __shared__ double sr[4];
   if ((threadIdx.x & 31) == 0) sr[threadIdx.x >> 5] = r;
@@ -440,7 +456,11 @@ __global__ void phase1_kernel(const double* __restrict__ centers, const double* 
   int bj[2] = {-1, -1};
   for (int J = threadIdx.x; J < T; J += blockDim.x) {
     if (same_single(trange, I, J)) continue;
-    double lb = tile_lb<M>(centers, radius, d, I, J);
+    // rank by distance from I's centre to J's ball (the tile itself first): the
+    // LB alone ties at 0 for every overlapping ball
+    double lb = (J == I) ? -INFINITY
+                         : metric_dist_real<M>(centers + (int64_t)I * d, centers + (int64_t)J * d, d) -
+                               radius[J];
     if (lb < bl[1] || (lb == bl[1] && J < bj[1])) {
       if (lb < bl[0] || (lb == bl[0] && J < bj[0])) {
         bl[1] = bl[0]; bj[1] = bj[0]; bl[0] = lb; bj[0] = J;
@@ -531,7 +551,7 @@ __global__ void tile_umax_kernel(const int* __restrict__ comp, int64_t n,
   const int T0 = blockIdx.x;
   int64_t i = (int64_t)T0 * TILE + threadIdx.x;
   double v = -INFINITY;
-  if (i < n) {
+  if (i < n && comp[i] >= 0) {
     unsigned long long u = U[comp[i]];
     v = (u == NONE_KEY) ? thr : fmin(bitsd(u), thr);
   }
@@ -597,19 +617,201 @@ __global__ void enum_write_kernel(const unsigned char* __restrict__ keep,
   }
 }
 
-__global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt, int64_t n,
-                                  unsigned long long* acc) {
+__global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt,
+                                  const int* __restrict__ tcount, unsigned long long* acc) {
   // real point pairs covered by a list of tile pairs (for the stats)
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long v = 0;
   if (t < cnt) {
     int2 it = items[t];
-    long long mI = n - (int64_t)it.x * TILE; if (mI > TILE) mI = TILE;
-    long long mJ = n - (int64_t)it.y * TILE; if (mJ > TILE) mJ = TILE;
+    long long mI = tcount[it.x], mJ = tcount[it.y];
     v = (it.x == it.y) ? (unsigned long long)(mI * (mI - 1) / 2) : (unsigned long long)(mI * mJ);
   }
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
   if ((threadIdx.x & 31) == 0 && v) atomicAdd(acc, v);
+}
+
+
+// ---- spatial order (kd bisection into 128-point leaves) ----------------------
+// Boruvka runs on a permuted copy in which every 128-point tile is a kd leaf
+// (spatially compact), so tile balls are tight and the pruning bound bites.
+// Keys that decide orders always use ORIGINAL indices (orig[] / pos[]).
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void kd_dim_kernel(const double* __restrict__ X64, int d, const int* __restrict__ order,
+                              const int* __restrict__ sbeg, const int* __restrict__ ssz, int nseg,
+                              int* __restrict__ sdim) {
+  const int sgm = blockIdx.x;
+  if (sgm >= nseg) return;
+  const int sz = ssz[sgm];
+  if (sz <= TILE) {
+    if (threadIdx.x == 0) sdim[sgm] = -1;
+    return;
+  }
+  const int b = sbeg[sgm];
+  // sample up to 64 evenly spaced points; spread per dimension
+  __shared__ float best[32];
+  __shared__ int bestk[32];
+  float bs = -1.f;
+  int bk = 0;
+  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+    float lo = INFINITY, hi = -INFINITY;
+    const int ns = sz < 64 ? sz : 64;
+    for (int t = 0; t < ns; ++t) {
+      const int p = b + (int)((long long)t * sz / ns);
+      const float v = (float)X64[(int64_t)order[p] * d + k];
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+    }
+    if (hi - lo > bs) {
+      bs = hi - lo;
+      bk = k;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    float os = __shfl_xor_sync(0xFFFFFFFFu, bs, o);
+    int ok = __shfl_xor_sync(0xFFFFFFFFu, bk, o);
+    if (os > bs || (os == bs && ok < bk)) {
+      bs = os;
+      bk = ok;
+    }
+  }
+  if (threadIdx.x == 0) sdim[sgm] = bk;
+}
+
+__global__ void kd_key_kernel(const double* __restrict__ X64, int64_t n, int d,
+                              const int* __restrict__ order, const int* __restrict__ segid,
+                              const int* __restrict__ sdim, unsigned long long* __restrict__ keys) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int sgm = segid[p];
+  const int k = sdim[sgm];
+  const uint32_t v = k >= 0 ? f2ord((float)X64[(int64_t)order[p] * d + k]) : 0u;
+  keys[p] = ((unsigned long long)(uint32_t)sgm << 32) | v;
+}
+
+// split position of each segment (sorted by the split coordinate): the largest
+// gap in the middle half if it is a real gap (>= 10% of the extent), else the
+// median.  Segments <= TILE are leaves.
+__global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
+                                   const int* __restrict__ sbeg, const int* __restrict__ ssz,
+                                   int nseg, int* __restrict__ ssplit) {
+  const int sgm = blockIdx.x;
+  if (sgm >= nseg) return;
+  const int sz = ssz[sgm], b = sbeg[sgm];
+  if (sz <= TILE) {
+    if (threadIdx.x == 0) ssplit[sgm] = sz;
+    return;
+  }
+  auto val = [&](int i) {
+    uint32_t u = (uint32_t)(keys[b + i] & 0xFFFFFFFFull);
+    u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+    return __uint_as_float(u);
+  };
+  const int lo = sz / 4, hi = sz - sz / 4;  // candidate cuts: left size in [lo, hi]
+  float bg = -1.f;
+  int bp = sz / 2;
+  for (int i = lo + threadIdx.x; i <= hi; i += blockDim.x) {
+    const float g = val(i) - val(i - 1);
+    if (g > bg || (g == bg && i < bp)) {
+      bg = g;
+      bp = i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    float og = __shfl_xor_sync(0xFFFFFFFFu, bg, o);
+    int op = __shfl_xor_sync(0xFFFFFFFFu, bp, o);
+    if (og > bg || (og == bg && op < bp)) {
+      bg = og;
+      bp = op;
+    }
+  }
+  if (threadIdx.x == 0) {
+    const float ext = val(sz - 1) - val(0);
+    ssplit[sgm] = (ext > 0.f && bg >= 0.1f * ext) ? bp : sz / 2;
+  }
+}
+
+__global__ void kd_children_kernel(int nseg, const int* __restrict__ ssz, int* __restrict__ nchild) {
+  int sgm = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sgm < nseg) nchild[sgm] = ssz[sgm] > TILE ? 2 : 1;
+}
+
+__global__ void kd_newsegs_kernel(int nseg, const int* __restrict__ sbeg, const int* __restrict__ ssz,
+                                  const int* __restrict__ ssplit, const int* __restrict__ cbase,
+                                  int* __restrict__ nbeg, int* __restrict__ nsz) {
+  int sgm = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sgm >= nseg) return;
+  const int c = cbase[sgm], sz = ssz[sgm], L = ssplit[sgm];
+  nbeg[c] = sbeg[sgm];
+  nsz[c] = L;
+  if (sz > TILE) {
+    nbeg[c + 1] = sbeg[sgm] + L;
+    nsz[c + 1] = sz - L;
+  }
+}
+
+__global__ void kd_relabel_kernel(int64_t n, const int* __restrict__ sbeg, const int* __restrict__ ssz,
+                                  const int* __restrict__ ssplit, const int* __restrict__ cbase,
+                                  int* __restrict__ segid) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int sgm = segid[p];
+  segid[p] = cbase[sgm] + ((ssz[sgm] > TILE && (int)(p - sbeg[sgm]) >= ssplit[sgm]) ? 1 : 0);
+}
+
+// compact order -> padded positions: leaf k occupies tile k
+__global__ void kd_place_kernel(int64_t n, const int* __restrict__ order, const int* __restrict__ segid,
+                                const int* __restrict__ sbeg, int* __restrict__ porig,
+                                int* __restrict__ ppos) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int sgm = segid[c];
+  const int64_t p = (int64_t)sgm * TILE + (c - sbeg[sgm]);
+  porig[p] = order[c];
+  ppos[order[c]] = (int)p;
+}
+
+__global__ void fill_int_kernel(int* a, int64_t n, int v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+__global__ void tile_count_kernel(const int* __restrict__ porig, int T, int* __restrict__ tcount) {
+  const int t = blockIdx.x;
+  int c = porig[(int64_t)t * TILE + threadIdx.x] >= 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  __shared__ int s[4];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) tcount[t] = s[0] + s[1] + s[2] + s[3];
+}
+
+__global__ void fill_comp_view_kernel(const int* __restrict__ porig, int64_t np, int* __restrict__ comp) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < np) comp[p] = porig[p] >= 0 ? (int)p : -1;
+}
+
+__global__ void gather_rows_kernel(const double* __restrict__ X64, int64_t n, int d,
+                                   const int* __restrict__ order, double* __restrict__ out) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * d) return;
+  int64_t p = t / d, k = t % d;
+  out[t] = order[p] >= 0 ? X64[(int64_t)order[p] * d + k] : 0.0;
+}
+
+__global__ void inverse_perm_kernel(int64_t n, const int* __restrict__ order, int* __restrict__ pos) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n && order[p] >= 0) pos[order[p]] = (int)p;
+}
+
+__global__ void gather_norm_kernel(int64_t n, const int* __restrict__ order,
+                                   const double* __restrict__ norm, double* __restrict__ out) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) out[p] = order[p] >= 0 ? norm[order[p]] : 0.0;
 }
 
 // ---- round path -----------------------------------------------------------
@@ -705,7 +907,7 @@ __global__ void tile_range_kernel(const int* __restrict__ comp, int64_t n, int T
   int t = blockIdx.x;
   int lo = 0x7FFFFFFF, hi = -0x7FFFFFFF;
   int64_t i = (int64_t)t * TILE + threadIdx.x;
-  if (i < n) {
+  if (i < n && comp[i] >= 0) {  // pads carry comp -1
     lo = comp[i];
     hi = lo;
   }
@@ -786,6 +988,22 @@ struct nnm_dataset {
   DevBuf<int2> pairs;
   DevBuf<double> pair_d;
   DevBuf<int> flag;
+  // Boruvka view: kd-ordered copy (positions p; orig[p] = original index)
+  bool have_order = false;
+  DevBuf<int> porig, ppos;
+  DevBuf<double> X64p, normp;
+  DevBuf<float> X32p;
+  double maxnormp = 0.0;
+  int normp_metric = -1;
+  int64_t np_ = 0;                  // positions of the Boruvka view (tiles x 128, pads included)
+  int Tp = 0;
+  DevBuf<int> tcount_p, tcount_o;   // real points per tile (Boruvka view / original)
+  // current view used by the shared helpers (scan / collect / exact_pairs)
+  const float* cur_X32 = nullptr;
+  const double* cur_X64 = nullptr;
+  int64_t vn = 0, vld = 0;
+  int vT = 0;
+  const int* cur_tcount = nullptr;
   // pruning
   int geom_metric = -1;
   DevBuf<double> tcenter, tradius, tumax;
@@ -843,7 +1061,33 @@ struct nnm_dataset {
     norm_metric = kind;
   }
 
-  int64_t tile_pairs() const { return (int64_t)T * (T + 1) / 2; }
+  int64_t tile_pairs() const { return (int64_t)vT * (vT + 1) / 2; }
+
+  void use_original_view() {
+    cur_X32 = X32.p;
+    cur_X64 = X64.p;
+    vn = n;
+    vld = ld;
+    vT = T;
+    if (!tcount_o.p) {
+      tcount_o.ensure(T);
+      std::vector<int> h(T);
+      for (int t = 0; t < T; ++t) h[t] = (int)std::min<int64_t>(TILE, n - (int64_t)t * TILE);
+      CUDA_TRY(cudaMemcpyAsync(tcount_o.p, h.data(), T * sizeof(int), cudaMemcpyHostToDevice, st));
+      sync();
+    }
+    cur_tcount = tcount_o.p;
+  }
+
+  void use_boruvka_view() {
+    ensure_order();
+    cur_X32 = X32p.p;
+    cur_X64 = X64p.p;
+    vn = np_;
+    vld = np_;
+    vT = Tp;
+    cur_tcount = tcount_p.p;
+  }
 
   static int size_rule(int kl2, int kl3) {
     if (kl3 != INT_UNSET) return kl3;
@@ -852,8 +1096,8 @@ struct nnm_dataset {
   }
 
   const int* eff_sizes(int kl2) {
-    psize_eff.ensure(ld);
-    eff_size_kernel<<<blocks_for(ld), 256, 0, st>>>(psize.p, ld, kl2, psize_eff.p); note_launch();
+    psize_eff.ensure(vld);
+    eff_size_kernel<<<blocks_for(vld), 256, 0, st>>>(psize.p, vld, kl2, psize_eff.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     return psize_eff.p;
   }
@@ -863,18 +1107,18 @@ struct nnm_dataset {
             float thr_hi, int64_t w_begin, int64_t w_end, const int2* items = nullptr,
             bool reset = true) {
     if (reset) {
-      fill_none(b1, n);
-      if (b2) fill_none(b2, n);
+      fill_none(b1, vn);
+      if (b2) fill_none(b2, vn);
     }
-    tile_range.ensure(T);
-    tile_range_kernel<<<T, TILE, 0, st>>>(comp.p, n, T, tile_range.p); note_launch();
+    tile_range.ensure(vT);
+    tile_range_kernel<<<vT, TILE, 0, st>>>(comp.p, vn, vT, tile_range.p); note_launch();
     const int ksum = size_rule(kl2, kl3);
     ScanArgs a;
-    a.X32 = X32.p;
-    a.ld = ld;
-    a.n = (int)n;
+    a.X32 = cur_X32;
+    a.ld = vld;
+    a.n = (int)vn;
     a.d = d;
-    a.T = T;
+    a.T = vT;
     a.comp = comp.p;
     a.psize = ksum != INT_UNSET ? eff_sizes(kl2) : comp.p;
     a.ksum = ksum;
@@ -901,7 +1145,7 @@ struct nnm_dataset {
     if (items) {  // exact count of real pairs in the listed tile pairs
       counters.ensure(8);
       CUDA_TRY(cudaMemsetAsync(counters.p + 7, 0, sizeof(unsigned long long), st));
-      item_pairs_kernel<<<blocks_for(w_end - w_begin), 256, 0, st>>>(items + w_begin, w_end - w_begin, n, counters.p + 7); note_launch();
+      item_pairs_kernel<<<blocks_for(w_end - w_begin), 256, 0, st>>>(items + w_begin, w_end - w_begin, cur_tcount, counters.p + 7); note_launch();
       stats.pairs_evaluated += (double)read1(counters.p + 7);
     } else {  // unordered real pairs covered by this range of the triangle
       stats.pairs_evaluated += (double)n * (double)(n - 1) / 2.0 * ((double)(w_end - w_begin) / (double)tile_pairs());
@@ -914,10 +1158,10 @@ struct nnm_dataset {
     if (nr <= 0 || nc_cols <= 0) return 0;
     int64_t ldr = ((int64_t)nr + TILE - 1) / TILE * TILE;
     gathered.ensure((size_t)ldr * d);
-    gather_kernel<<<blocks_for(ldr), 256, 0, st>>>(X32.p, ld, d, rows, nr, ldr, gathered.p); note_launch();
+    gather_kernel<<<blocks_for(ldr), 256, 0, st>>>(cur_X32, vld, d, rows, nr, ldr, gathered.p); note_launch();
     CUDA_TRY(cudaGetLastError());
-    const float* XC = X32.p;
-    int64_t ldc = ld;
+    const float* XC = cur_X32;
+    int64_t ldc = vld;
     DevBuf<float> gcols;
     if (cols) {
       ldc = ((int64_t)nc_cols + TILE - 1) / TILE * TILE;
@@ -926,7 +1170,7 @@ struct nnm_dataset {
         ldc = ldr;
       } else {
         gcols.ensure((size_t)ldc * d);
-        gather_kernel<<<blocks_for(ldc), 256, 0, st>>>(X32.p, ld, d, cols, nc_cols, ldc, gcols.p); note_launch();
+        gather_kernel<<<blocks_for(ldc), 256, 0, st>>>(cur_X32, vld, d, cols, nc_cols, ldc, gcols.p); note_launch();
         CUDA_TRY(cudaGetLastError());
         XC = gcols.p;
       }
@@ -971,13 +1215,13 @@ struct nnm_dataset {
     if (count == 0) return;
     switch (metric) {
       case MANHATTAN:
-        exact_pairs_kernel<MANHATTAN><<<blocks_for(count), 256, 0, st>>>(X64.p, d, pairs.p, count, pair_d.p); note_launch();
+        exact_pairs_kernel<MANHATTAN><<<blocks_for(count), 256, 0, st>>>(cur_X64, d, pairs.p, count, pair_d.p); note_launch();
         break;
       case CHEBYSHEV:
-        exact_pairs_kernel<CHEBYSHEV><<<blocks_for(count), 256, 0, st>>>(X64.p, d, pairs.p, count, pair_d.p); note_launch();
+        exact_pairs_kernel<CHEBYSHEV><<<blocks_for(count), 256, 0, st>>>(cur_X64, d, pairs.p, count, pair_d.p); note_launch();
         break;
       default:
-        exact_pairs_kernel<EUCLIDEAN><<<blocks_for(count), 256, 0, st>>>(X64.p, d, pairs.p, count, pair_d.p); note_launch();
+        exact_pairs_kernel<EUCLIDEAN><<<blocks_for(count), 256, 0, st>>>(cur_X64, d, pairs.p, count, pair_d.p); note_launch();
     }
     CUDA_TRY(cudaGetLastError());
     stats.exact_evals += count;
@@ -986,7 +1230,8 @@ struct nnm_dataset {
   // ---------------------------------------------------------------- Boruvka
   void bv_begin(int metric, double dmax) {
     bv_metric = metric;
-    ensure_norms(metric);
+    use_boruvka_view();
+    ensure_norms_p(metric);
     em = make_err_model(metric, d);
     bv_thr = INFINITY;
     bv_thr_hi = INFINITY;
@@ -994,18 +1239,20 @@ struct nnm_dataset {
       bv_thr = metric == EUCLIDEAN ? dmax * dmax : dmax;  // metrics.py:93-103
       bv_thr_hi = float_up(screen_upper(em, bv_thr, 2.0 * maxnorm));
     }
-    comp.ensure(ld);
-    fill_comp_kernel<<<blocks_for(ld), 256, 0, st>>>(comp.p, nullptr, n, ld); note_launch();
+    comp.ensure(vn);
+    fill_comp_view_kernel<<<blocks_for(vn), 256, 0, st>>>(porig.p, vn, comp.p); note_launch();
     CUDA_TRY(cudaGetLastError());
-    rb_d.ensure(n);
-    rb_j.ensure(n);
-    rowlow.ensure(n);
-    amb.ensure(n);
-    resc.ensure(n);
-    resc_bound.ensure(n);
-    parent.ensure(n);
-    cmin_d.ensure(n);
-    cmin_ab.ensure(n);
+    B1.ensure(vn);
+    B2.ensure(vn);
+    rb_d.ensure(vn);
+    rb_j.ensure(vn);
+    rowlow.ensure(vn);
+    amb.ensure(vn);
+    resc.ensure(vn);
+    resc_bound.ensure(vn);
+    parent.ensure(vn);
+    cmin_d.ensure(vn);
+    cmin_ab.ensure(vn);
     counters.ensure(8);
     edges.ensure(std::max<int64_t>(n - 1, 1));
     flag.ensure(1);
@@ -1014,16 +1261,110 @@ struct nnm_dataset {
     bv_ncomp = n;
   }
 
+  void ensure_order() {
+    if (have_order) return;
+    // compact kd order over the n real points
+    DevBuf<int> order, segid;
+    order.ensure(n);
+    segid.ensure(n);
+    iota_kernel<<<blocks_for(n), 256, 0, st>>>(order.p, (int)n); note_launch();
+    CUDA_TRY(cudaMemsetAsync(segid.p, 0, n * sizeof(int), st));
+    std::vector<int> hb = {0}, hs = {(int)n};
+    int nseg = 1;
+    const char* ke = getenv("NNM_KD");
+    const bool kd = n > TILE && !(ke && ke[0] == '0');
+    DevBuf<int> sbeg, ssz;
+    sbeg.ensure(1);
+    ssz.ensure(1);
+    CUDA_TRY(cudaMemcpyAsync(sbeg.p, hb.data(), sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ssz.p, hs.data(), sizeof(int), cudaMemcpyHostToDevice, st));
+    if (!kd) {  // no reordering: cut the original order into 128-point leaves
+      nseg = (int)((n + TILE - 1) / TILE);
+      hb.resize(nseg);
+      hs.resize(nseg);
+      for (int t = 0; t < nseg; ++t) {
+        hb[t] = t * TILE;
+        hs[t] = (int)std::min<int64_t>(TILE, n - (int64_t)t * TILE);
+      }
+      std::vector<int> hseg(n);
+      for (int64_t c = 0; c < n; ++c) hseg[c] = (int)(c / TILE);
+      sbeg.ensure(nseg);
+      ssz.ensure(nseg);
+      CUDA_TRY(cudaMemcpyAsync(sbeg.p, hb.data(), nseg * sizeof(int), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(ssz.p, hs.data(), nseg * sizeof(int), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(segid.p, hseg.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+      sync();
+    } else {
+      DevBuf<int> sdim, ssplit, nchild, cbase, nbeg, nsz;
+      DevBuf<unsigned long long> keys;
+      keys.ensure(n);
+      for (int lv = 0; lv < 64; ++lv) {
+        std::vector<int> hsz(nseg);
+        CUDA_TRY(cudaMemcpyAsync(hsz.data(), ssz.p, nseg * sizeof(int), cudaMemcpyDeviceToHost, st));
+        sync();
+        if (*std::max_element(hsz.begin(), hsz.end()) <= TILE) break;
+        sdim.ensure(nseg);
+        ssplit.ensure(nseg);
+        nchild.ensure(nseg);
+        cbase.ensure(nseg + 1);
+        kd_dim_kernel<<<nseg, 32, 0, st>>>(X64.p, d, order.p, sbeg.p, ssz.p, nseg, sdim.p); note_launch();
+        kd_key_kernel<<<blocks_for(n), 256, 0, st>>>(X64.p, n, d, order.p, segid.p, sdim.p, keys.p); note_launch();
+        thrust::stable_sort_by_key(thrust::cuda::par.on(st), keys.p, keys.p + n, order.p);
+        kd_splitpos_kernel<<<nseg, 32, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, ssplit.p); note_launch();
+        kd_children_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, ssz.p, nchild.p); note_launch();
+        thrust::exclusive_scan(thrust::cuda::par.on(st), nchild.p, nchild.p + nseg, cbase.p, 0);
+        int lastc = read1(nchild.p + (nseg - 1)), lastb = read1(cbase.p + (nseg - 1));
+        const int nseg2 = lastb + lastc;
+        nbeg.ensure(nseg2);
+        nsz.ensure(nseg2);
+        kd_newsegs_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, sbeg.p, ssz.p, ssplit.p, cbase.p, nbeg.p, nsz.p); note_launch();
+        kd_relabel_kernel<<<blocks_for(n), 256, 0, st>>>(n, sbeg.p, ssz.p, ssplit.p, cbase.p, segid.p); note_launch();
+        CUDA_TRY(cudaGetLastError());
+        std::swap(sbeg.p, nbeg.p);
+        std::swap(sbeg.n, nbeg.n);
+        std::swap(ssz.p, nsz.p);
+        std::swap(ssz.n, nsz.n);
+        nseg = nseg2;
+      }
+    }
+    // leaf k -> tile k (positions k*128 .. k*128 + size - 1, then pads)
+    Tp = nseg;
+    np_ = (int64_t)Tp * TILE;
+    porig.ensure(np_);
+    ppos.ensure(n);
+    fill_int_kernel<<<blocks_for(np_), 256, 0, st>>>(porig.p, np_, -1); note_launch();
+    kd_place_kernel<<<blocks_for(n), 256, 0, st>>>(n, order.p, segid.p, sbeg.p, porig.p, ppos.p); note_launch();
+    tcount_p.ensure(Tp);
+    tile_count_kernel<<<Tp, TILE, 0, st>>>(porig.p, Tp, tcount_p.p); note_launch();
+    X64p.ensure((size_t)np_ * d);
+    gather_rows_kernel<<<blocks_for(np_ * d), 256, 0, st>>>(X64.p, np_, d, porig.p, X64p.p); note_launch();
+    X32p.ensure((size_t)np_ * d);
+    CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    prepare_view_kernel<<<blocks_for(np_), 256, 0, st>>>(X64p.p, porig.p, np_, d, X32p.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    sync();
+    have_order = true;
+  }
+
+  void ensure_norms_p(int metric) {
+    ensure_norms(metric);
+    if (normp_metric == norm_metric) return;
+    normp.ensure(np_);
+    gather_norm_kernel<<<blocks_for(np_), 256, 0, st>>>(np_, porig.p, norm.p, normp.p); note_launch();
+    maxnormp = maxnorm;
+    normp_metric = norm_metric;
+  }
+
   void ensure_geometry(int metric) {
     int kind = (metric == SQEUCLIDEAN) ? EUCLIDEAN : metric;
     if (geom_metric == kind) return;
-    tcenter.ensure((size_t)T * d);
-    tradius.ensure(T);
+    tcenter.ensure((size_t)Tp * d);
+    tradius.ensure(Tp);
     size_t sm = (size_t)d * sizeof(double);
     switch (kind) {
-      case MANHATTAN: tile_geom_kernel<MANHATTAN><<<T, TILE, sm, st>>>(X64.p, n, d, tcenter.p, tradius.p); break;
-      case CHEBYSHEV: tile_geom_kernel<CHEBYSHEV><<<T, TILE, sm, st>>>(X64.p, n, d, tcenter.p, tradius.p); break;
-      default: tile_geom_kernel<EUCLIDEAN><<<T, TILE, sm, st>>>(X64.p, n, d, tcenter.p, tradius.p);
+      case MANHATTAN: tile_geom_kernel<MANHATTAN><<<Tp, TILE, sm, st>>>(X64p.p, tcount_p.p, d, tcenter.p, tradius.p); break;
+      case CHEBYSHEV: tile_geom_kernel<CHEBYSHEV><<<Tp, TILE, sm, st>>>(X64p.p, tcount_p.p, d, tcenter.p, tradius.p); break;
+      default: tile_geom_kernel<EUCLIDEAN><<<Tp, TILE, sm, st>>>(X64p.p, tcount_p.p, d, tcenter.p, tradius.p);
     }
     note_launch();
     CUDA_TRY(cudaGetLastError());
@@ -1034,13 +1375,13 @@ struct nnm_dataset {
   void pruned_lists(int64_t& n1, int64_t& n2) {
     const int64_t W = tile_pairs();
     // phase-1 seeds: PK nearest cross-capable tiles per tile
-    items1.ensure((size_t)T * PK);
-    phase1_kernel<M><<<T, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, T, d, items1.p); note_launch();
+    items1.ensure((size_t)Tp * PK);
+    phase1_kernel<M><<<Tp, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, Tp, d, items1.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     auto* k64 = reinterpret_cast<unsigned long long*>(items1.p);  // (I, J) -> J << 32 | I order
     // sort by (I, J): int2 memory is {x=I, y=J}; as u64 little-endian = J << 32 | I -> swap to key
-    thrust::sort(thrust::cuda::par.on(st), k64, k64 + (size_t)T * PK, ItemLess());
-    auto* end = thrust::unique(thrust::cuda::par.on(st), k64, k64 + (size_t)T * PK);
+    thrust::sort(thrust::cuda::par.on(st), k64, k64 + (size_t)Tp * PK, ItemLess());
+    auto* end = thrust::unique(thrust::cuda::par.on(st), k64, k64 + (size_t)Tp * PK);
     n1 = end - k64;
     // drop the (-1,-1) padding, which sorts first
     int2 first = read1(items1.p);
@@ -1049,7 +1390,7 @@ struct nnm_dataset {
     int2* list1 = items1.p + skip;
     pbits.ensure((size_t)(W + 31) / 32);
     CUDA_TRY(cudaMemsetAsync(pbits.p, 0, ((W + 31) / 32) * sizeof(unsigned), st));
-    if (n1 > 0) { mark_items_kernel<<<blocks_for(n1), 256, 0, st>>>(list1, n1, T, pbits.p); note_launch(); }
+    if (n1 > 0) { mark_items_kernel<<<blocks_for(n1), 256, 0, st>>>(list1, n1, Tp, pbits.p); note_launch(); }
     p1_list = list1;
     (void)W;
     n2 = 0;
@@ -1058,45 +1399,45 @@ struct nnm_dataset {
   template <int M>
   void pruned_phase2(int64_t& n2) {
     const int64_t W = tile_pairs();
-    tumax.ensure(T);
-    tile_umax_kernel<<<T, TILE, 0, st>>>(comp.p, n, ucomp.p, bv_thr, tumax.p); note_launch();
+    tumax.ensure(Tp);
+    tile_umax_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, ucomp.p, bv_thr, tumax.p); note_launch();
     pkeep.ensure(W);
-    pcount.ensure(T);
-    poffset.ensure(T + 1);
-    enum_count_kernel<M><<<T, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, tumax.p, pbits.p, T, d,
+    pcount.ensure(Tp);
+    poffset.ensure(Tp + 1);
+    enum_count_kernel<M><<<Tp, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, tumax.p, pbits.p, Tp, d,
                                              pkeep.p, pcount.p); note_launch();
     CUDA_TRY(cudaGetLastError());
-    thrust::exclusive_scan(thrust::cuda::par.on(st), pcount.p, pcount.p + T, poffset.p, 0LL);
-    long long last_off = read1(poffset.p + (T - 1));
-    int last_cnt = read1(pcount.p + (T - 1));
+    thrust::exclusive_scan(thrust::cuda::par.on(st), pcount.p, pcount.p + Tp, poffset.p, 0LL);
+    long long last_off = read1(poffset.p + (Tp - 1));
+    int last_cnt = read1(pcount.p + (Tp - 1));
     n2 = last_off + last_cnt;
     items2.ensure(std::max<int64_t>(n2, 1));
-    if (n2 > 0) { enum_write_kernel<<<T, 256, 0, st>>>(pkeep.p, poffset.p, T, items2.p); note_launch(); }
+    if (n2 > 0) { enum_write_kernel<<<Tp, 256, 0, st>>>(pkeep.p, poffset.p, Tp, items2.p); note_launch(); }
     CUDA_TRY(cudaGetLastError());
   }
 
   template <int M>
   void ucomp_t(const unsigned long long* b1) {
-    ucomp_kernel<M><<<blocks_for(n), 256, 0, st>>>(X64.p, (int)n, d, b1, comp.p, bv_thr, ucomp.p); note_launch();
+    ucomp_kernel<M><<<blocks_for(vn), 256, 0, st>>>(X64p.p, (int)vn, d, b1, comp.p, bv_thr, ucomp.p); note_launch();
   }
 
   // One pruned Boruvka scan: exact per-row keys for every row that can hold its
   // component's minimum edge.
   void pruned_scan(int metric) {
     ensure_geometry(metric);
-    tile_range.ensure(T);
-    tile_range_kernel<<<T, TILE, 0, st>>>(comp.p, n, T, tile_range.p); note_launch();
+    tile_range.ensure(Tp);
+    tile_range_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, Tp, tile_range.p); note_launch();
     int64_t n1 = 0, n2 = 0;
     switch (metric) {
       case MANHATTAN: pruned_lists<MANHATTAN>(n1, n2); break;
       case CHEBYSHEV: pruned_lists<CHEBYSHEV>(n1, n2); break;
       default: pruned_lists<EUCLIDEAN>(n1, n2);
     }
-    fill_none(B1.p, n);
-    fill_none(B2.p, n);
+    fill_none(B1.p, vn);
+    fill_none(B2.p, vn);
     if (n1 > 0) scan(metric, B1.p, B2.p, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
-    ucomp.ensure(n);
-    fill_none(ucomp.p, n);
+    ucomp.ensure(vn);
+    fill_none(ucomp.p, vn);
     switch (metric) {
       case MANHATTAN: ucomp_t<MANHATTAN>(B1.p); pruned_phase2<MANHATTAN>(n2); break;
       case CHEBYSHEV: ucomp_t<CHEBYSHEV>(B1.p); pruned_phase2<CHEBYSHEV>(n2); break;
@@ -1104,17 +1445,57 @@ struct nnm_dataset {
     }
     if (n2 > 0) scan(metric, B1.p, B2.p, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n2, items2.p, false);
     pairs_covered += (double)n * (double)(n - 1) / 2.0;
+    if (getenv("NNM_DEBUG")) {
+      const int T = Tp;
+      std::vector<double> rad(T), um(T);
+      CUDA_TRY(cudaMemcpyAsync(rad.data(), tradius.p, T * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(um.data(), tumax.p, T * sizeof(double), cudaMemcpyDeviceToHost, st));
+      sync();
+      std::vector<double> r2 = rad, u2 = um;
+      std::sort(r2.begin(), r2.end());
+      std::sort(u2.begin(), u2.end());
+      int ninf = 0;
+      for (double u : um) ninf += std::isinf(u);
+      {
+        const int64_t n = vn;
+        std::vector<unsigned long long> uc(n), b1(n);
+        std::vector<int> cp(n);
+        CUDA_TRY(cudaMemcpyAsync(uc.data(), ucomp.p, n * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(cp.data(), comp.p, n * 4, cudaMemcpyDeviceToHost, st));
+        sync();
+        std::vector<double> uv;
+        int64_t none = 0;
+        for (int64_t i = 0; i < n; ++i) {
+          if (cp[i] < 0) continue;
+          unsigned long long u = uc[cp[i]];
+          if (u == NONE_KEY) ++none; else uv.push_back(bits_to_double(u));
+        }
+        std::sort(uv.begin(), uv.end());
+        if (!uv.empty())
+          fprintf(stderr, "[nnm]   point U: p10 %.3g p50 %.3g p90 %.3g p99 %.3g none %lld\n", uv[uv.size() / 10],
+                  uv[uv.size() / 2], uv[uv.size() * 9 / 10], uv[uv.size() * 99 / 100], (long long)none);
+        std::vector<int2> it1(n1);
+        CUDA_TRY(cudaMemcpyAsync(it1.data(), p1_list, n1 * sizeof(int2), cudaMemcpyDeviceToHost, st));
+        sync();
+        int64_t diag = 0;
+        for (auto& q : it1) diag += (q.x == q.y);
+        fprintf(stderr, "[nnm]   phase1 diag items %lld\n", (long long)diag);
+      }
+      fprintf(stderr, "[nnm] round %d: phase1 %lld items, phase2 %lld of %lld tile pairs (%.3f%%); radius p50 %.3g p90 %.3g max %.3g; umax p50 %.3g p90 %.3g inf %d/%d\n",
+              bv_round + 1, (long long)n1, (long long)n2, (long long)tile_pairs(), 100.0 * n2 / tile_pairs(),
+              r2[T / 2], r2[T * 9 / 10], r2[T - 1], u2[T / 2], u2[T * 9 / 10], ninf, T);
+    }
   }
 
   template <int M>
   void refine_t(const unsigned long long* b1, const unsigned long long* b2) {
-    refine_kernel<M><<<blocks_for(n), 256, 0, st>>>(X64.p, (int)n, d, b1, b2, norm.p, maxnorm, em,
+    refine_kernel<M><<<blocks_for(vn), 256, 0, st>>>(X64p.p, (int)vn, d, b1, b2, normp.p, maxnormp, em,
                                                     bv_thr, rb_d.p, rb_j.p, rowlow.p, amb.p,
-                                                    counters.p + 1); note_launch();
+                                                    counters.p + 1, porig.p); note_launch();
   }
 
   int64_t bv_finish_round(const unsigned long long* b1, const unsigned long long* b2) {
-    const int N = (int)n;
+    const int N = (int)vn;  // positions of the Boruvka view (pads carry comp -1)
     ++bv_round;
     // counters[0]: edges (cumulative), [1]: ambiguous, [2]: rescan rows
     CUDA_TRY(cudaMemsetAsync(counters.p + 1, 0, 2 * sizeof(unsigned long long), st));
@@ -1124,14 +1505,14 @@ struct nnm_dataset {
       default: refine_t<EUCLIDEAN>(b1, b2);
     }
     CUDA_TRY(cudaGetLastError());
-    fill_none(cmin_d.p, n);
-    compmin_d_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, rb_d.p, cmin_d.p); note_launch();
+    fill_none(cmin_d.p, vn);
+    compmin_d_kernel<<<blocks_for(vn), 256, 0, st>>>(N, comp.p, rb_d.p, cmin_d.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     unsigned long long n_amb = read1(counters.p + 1);
     stats.ambiguous_rows += (int64_t)n_amb;
     if (n_amb > 0) {
       amb_filter_kernel<<<blocks_for(n_amb), 256, 0, st>>>(amb.p, (int)n_amb, comp.p, rowlow.p,
-                                                         cmin_d.p, rb_d.p, bv_thr, norm.p, maxnorm,
+                                                         cmin_d.p, rb_d.p, bv_thr, normp.p, maxnormp,
                                                          em, resc.p, resc_bound.p, counters.p + 2); note_launch();
       CUDA_TRY(cudaGetLastError());
       unsigned long long n_res = read1(counters.p + 2);
@@ -1143,28 +1524,28 @@ struct nnm_dataset {
         if (np > 0) {
           rowmin_d_kernel<<<blocks_for(np), 256, 0, st>>>(pairs.p, pair_d.p, np, bv_thr, rb_d.p); note_launch();
           rowmin_j_kernel<<<blocks_for(np), 256, 0, st>>>(pairs.p, pair_d.p, np, bv_thr, rb_d.p,
-                                                          rb_j.p); note_launch();
+                                                          rb_j.p, porig.p); note_launch();
         }
         fix_rows_kernel<<<blocks_for(n_res), 256, 0, st>>>(resc.p, (int)n_res, rb_d.p, rb_j.p); note_launch();
         CUDA_TRY(cudaGetLastError());
         // recompute component minima with the resolved rows
-        fill_none(cmin_d.p, n);
-        compmin_d_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, rb_d.p, cmin_d.p); note_launch();
+        fill_none(cmin_d.p, vn);
+        compmin_d_kernel<<<blocks_for(vn), 256, 0, st>>>(N, comp.p, rb_d.p, cmin_d.p); note_launch();
       }
     }
-    fill_none(cmin_ab.p, n);
-    compmin_ab_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, rb_d.p, rb_j.p, cmin_d.p, cmin_ab.p); note_launch();
+    fill_none(cmin_ab.p, vn);
+    compmin_ab_kernel<<<blocks_for(vn), 256, 0, st>>>(N, comp.p, rb_d.p, rb_j.p, cmin_d.p, cmin_ab.p, porig.p); note_launch();
     unsigned long long before = read1(counters.p);
-    hook_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, cmin_d.p, cmin_ab.p, parent.p, edges.p,
-                                               counters.p, bv_round); note_launch();
+    hook_kernel<<<blocks_for(vn), 256, 0, st>>>(N, comp.p, cmin_d.p, cmin_ab.p, parent.p, edges.p,
+                                               counters.p, bv_round, ppos.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     for (int it = 0; it < 64; ++it) {
       CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
-      jump_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, parent.p, flag.p); note_launch();
+      jump_kernel<<<blocks_for(vn), 256, 0, st>>>(N, comp.p, parent.p, flag.p); note_launch();
       CUDA_TRY(cudaGetLastError());
       if (read1(flag.p) == 0) break;
     }
-    relabel_kernel<<<blocks_for(n), 256, 0, st>>>(N, comp.p, parent.p); note_launch();
+    relabel_kernel<<<blocks_for(vn), 256, 0, st>>>(N, comp.p, parent.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     unsigned long long after = read1(counters.p);
     int64_t added = (int64_t)(after - before);
@@ -1242,6 +1623,7 @@ struct nnm_dataset {
 
   void top_p(int metric, double thr, int kl2, int kl3, int64_t P, std::vector<Cand>& out) {
     ensure_norms(metric);
+    use_original_view();
     em = make_err_model(metric, d);
     float thr_hi = std::isinf(thr) ? INFINITY : float_up(screen_upper(em, thr, 2.0 * maxnorm));
     B1.ensure(n);
@@ -1499,8 +1881,6 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       // ---------------- Boruvka: exact MST of the eligible graph, then replay
       ds->stats.path = NNM_PATH_BORUVKA;
       ds->bv_begin(metric, cons->dmax);
-      ds->B1.ensure(n);
-      ds->B2.ensure(n);
       bool need = n > 1 && !(cons->kl1 > 0 && n <= cons->kl1);
       const char* pe = getenv("NNM_PRUNE");
       const bool prune = !(pe && pe[0] == '0');
@@ -1645,7 +2025,8 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
 }
 
 // ---- staged Boruvka API (multi-GPU driver) ----------------------------------
-int nnm_bv_begin(nnm_dataset* ds, int32_t metric, double dmax, int64_t* out_tile_pairs) {
+int nnm_bv_begin(nnm_dataset* ds, int32_t metric, double dmax, int64_t* out_tile_pairs,
+                 int64_t* out_rows) {
   return guarded([&] {
     if (!ds) invalid("null dataset");
     check_metric(metric);
@@ -1655,6 +2036,7 @@ int nnm_bv_begin(nnm_dataset* ds, int32_t metric, double dmax, int64_t* out_tile
     ds->stats.path = NNM_PATH_BORUVKA;
     ds->bv_begin(metric, dmax);
     if (out_tile_pairs) *out_tile_pairs = ds->tile_pairs();
+    if (out_rows) *out_rows = ds->vn;
   });
 }
 

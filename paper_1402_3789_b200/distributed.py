@@ -69,19 +69,21 @@ def run_boruvka_distributed_handle(dd, *, metric="euclidean", dmax=None, kl1=Non
     t0 = time.perf_counter()
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
-    tp = ctypes.c_int64()
+    tp, rows = ctypes.c_int64(), ctypes.c_int64()
     _native.check(lib.nnm_bv_begin(dd.handle, metric_code(metric),
-                                   np.nan if dmax is None else float(dmax), ctypes.byref(tp)))
+                                   np.nan if dmax is None else float(dmax), ctypes.byref(tp),
+                                   ctypes.byref(rows)))
     n = dd.n
     lo, hi = shard_range(tp.value, rank, world)
-    b1 = torch.empty(n, dtype=torch.int64, device="cuda")
-    b2 = torch.empty(n, dtype=torch.int64, device="cuda")
+    b1 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
+    b2 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
     g1 = torch.empty_like(b1)
     c2 = torch.empty_like(b1)
     added = ctypes.c_int64()
     need = n > 1 and not (kl1 is not None and n <= kl1)
     while need:
         _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
+        torch.cuda.synchronize()
         g1.copy_(b1)
         dist.all_reduce(g1, op=dist.ReduceOp.MIN, group=group)
         _native.check(lib.nnm_bv_second(dd.handle, b1.data_ptr(), b2.data_ptr(), g1.data_ptr(),

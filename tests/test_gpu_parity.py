@@ -155,8 +155,8 @@ def test_staged_multi_range_equals_single(nnm):
     want = nnm.fit(X)
     lib = _native.load()
     dd = _native.DeviceDataset(X)
-    tp = ctypes.c_int64()
-    _native.check(lib.nnm_bv_begin(dd.handle, 0, np.nan, ctypes.byref(tp)))
+    tp, rows = ctypes.c_int64(), ctypes.c_int64()
+    _native.check(lib.nnm_bv_begin(dd.handle, 0, np.nan, ctypes.byref(tp), ctypes.byref(rows)))
     import torch
 
     n = X.shape[0]
@@ -165,10 +165,11 @@ def test_staged_multi_range_equals_single(nnm):
         parts = []
         for r in range(R):
             lo, hi = shard_range(tp.value, r, R)
-            b1 = torch.empty(n, dtype=torch.int64, device="cuda")
-            b2 = torch.empty(n, dtype=torch.int64, device="cuda")
+            b1 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
+            b2 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
             _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
             parts.append((b1, b2))
+        torch.cuda.synchronize()
         g1 = torch.stack([p[0] for p in parts]).min(0).values
         c2 = []
         for b1, b2 in parts:
@@ -177,6 +178,7 @@ def test_staged_multi_range_equals_single(nnm):
                                             out.data_ptr()))
             c2.append(out)
         g2 = torch.stack(c2).min(0).values
+        torch.cuda.synchronize()
         added = ctypes.c_int64()
         _native.check(lib.nnm_bv_finish_round(dd.handle, g1.data_ptr(), g2.data_ptr(),
                                               ctypes.byref(added)))
@@ -191,3 +193,34 @@ def test_staged_multi_range_equals_single(nnm):
     for f in FIELDS + ("round",):
         assert np.array_equal(merges[: nm.value][f], want.merges.array[f]), f
     assert np.array_equal(assign, want.assignments)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 127, 129, 300, 2049])
+def test_boruvka_small_and_ragged_sizes(nnm, n):
+    from oracle import nnm_oracle as orc
+
+    rng = np.random.default_rng(n)
+    X = rng.normal(size=(n, 3)) * 2.0
+    for metric in ("euclidean", "manhattan"):
+        m_or, a_or = orc.single_linkage(X, metric=metric)
+        res = nnm.fit(X, metric=metric)
+        got = _records(res.merges)
+        assert len(got) == len(m_or)
+        for f in FIELDS:
+            assert np.array_equal(got[f], m_or[f]), (metric, f)
+        assert np.array_equal(res.assignments, a_or)
+
+
+def test_boruvka_shuffled_blobs_vs_oracle(nnm):
+    """Row-shuffled blob data (SURVEY 8d asks for a shuffled variant): kd order + pruning."""
+    from oracle import nnm_oracle as orc
+
+    X = nnm.generate_synthetic(4000, 9, 23, 1.0, seed=7)[0]
+    X = X[np.random.default_rng(107).permutation(len(X))]
+    for cons in ({}, {"dmax": 4.0}, {"kl1": 5}):
+        m_or, a_or = orc.single_linkage(X, **cons)
+        res = nnm.fit(X, **cons)
+        got = _records(res.merges)
+        for f in FIELDS:
+            assert np.array_equal(got[f], m_or[f]), (cons, f)
+        assert np.array_equal(res.assignments, a_or)
