@@ -695,7 +695,7 @@ __global__ void kd_key_kernel(const double* __restrict__ X64, int64_t n, int d,
 
 // split position of each segment (sorted by the split coordinate): the largest
 // gap in the middle half if it is a real gap (>= 10% of the extent), else the
-// median.  Segments <= TILE are leaves.
+// multiple of 128 nearest the median.  Segments <= TILE are leaves.
 __global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
                                    const int* __restrict__ sbeg, const int* __restrict__ ssz,
                                    int nseg, int* __restrict__ ssplit) {
@@ -730,8 +730,13 @@ __global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
     }
   }
   if (threadIdx.x == 0) {
+    // no real gap: cut at the multiple of 128 nearest the median, so compact
+    // clusters fill whole tiles (few pad slots)
     const float ext = val(sz - 1) - val(0);
-    ssplit[sgm] = (ext > 0.f && bg >= 0.1f * ext) ? bp : sz / 2;
+    int L = ((sz + TILE) / (2 * TILE)) * TILE;
+    if (L < TILE) L = TILE;
+    if (L > sz - 1) L = sz - 1;
+    ssplit[sgm] = (ext > 0.f && bg >= 0.1f * ext) ? bp : L;
   }
 }
 
