@@ -627,10 +627,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
         for (int h = 0; h < 2; ++h) {
           uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
           uint32_t thr = gthr | 63u;
-#pragma unroll
+#pragma unroll 4
           for (int qq = 0; qq < 16; ++qq) {
-            // logical chunk q (compile-time) sits at position q ^ tt: distinct
-            // positions across the warp keep the LDS.128 bank-conflict free
+            // logical chunk q sits at position q ^ tt: distinct positions across
+            // the warp keep the LDS.128 bank-conflict free
             const int q = h * 16 + qq;
             const float4 v4 = *reinterpret_cast<const float4*>(Drow + ((q ^ tt) << 2));
             const uint32_t b0 = __float_as_uint(v4.x), b1 = __float_as_uint(v4.y);
@@ -638,8 +638,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
             const uint32_t mn = min(umin3(b0, b1, b2), b3);
             if (__any_sync(0xFFFFFFFFu, mn <= thr)) {
               const uint32_t bb[4] = {b0, b1, b2, b3};
-              int4 c4 = make_int4(0, 0, 0, 0), s4 = make_int4(0, 0, 0, 0);
-              if (may_share) c4 = *reinterpret_cast<const int4*>(cc + q * 4);
+              int4 s4 = make_int4(0, 0, 0, 0);
+              const int4 c4 = *reinterpret_cast<const int4*>(cc + q * 4);
               if (SIZES) s4 = *reinterpret_cast<const int4*>(sc + q * 4);
               const int ca[4] = {c4.x, c4.y, c4.z, c4.w};
               const int sa[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -647,8 +647,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
               uint32_t kk[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                bool ok = true;
-                if (may_share) ok = ca[e] != myC;
+                bool ok = ca[e] != myC;
                 if (SIZES) ok = ok && (myS + sa[e] <= p.ksum);
                 if (THR) ok = ok && (__uint_as_float(bb[e]) <= p.thr_hi);
                 const uint32_t bits = ok ? bb[e] : INF_BITS;
@@ -688,8 +687,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
             }
             const uint32_t mn = min(umin3(bb[0], bb[1], bb[2]), bb[3]);
             if (__any_sync(0xFFFFFFFFu, mn <= thr)) {
-              int4 c4 = make_int4(0, 0, 0, 0), s4 = make_int4(0, 0, 0, 0);
-              if (may_share) c4 = *reinterpret_cast<const int4*>(cr + r4 * 4);
+              int4 s4 = make_int4(0, 0, 0, 0);
+              const int4 c4 = *reinterpret_cast<const int4*>(cr + r4 * 4);
               if (SIZES) s4 = *reinterpret_cast<const int4*>(sr + r4 * 4);
               const int ca[4] = {c4.x, c4.y, c4.z, c4.w};
               const int sa[4] = {s4.x, s4.y, s4.z, s4.w};
@@ -697,8 +696,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int r = r4 * 4 + u;
-                bool ok = true;
-                if (may_share) ok = ca[u] != myC;
+                bool ok = ca[u] != myC;
                 if (SIZES) ok = ok && (myS + sa[u] <= p.ksum);
                 if (THR) ok = ok && (__uint_as_float(bb[u]) <= p.thr_hi);
                 const uint32_t bits = ok ? bb[u] : INF_BITS;
