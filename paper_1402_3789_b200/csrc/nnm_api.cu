@@ -198,7 +198,7 @@ __global__ void refine_kernel(const double* __restrict__ X64, int n, int d,
                               const double* __restrict__ norm, double maxnorm, ErrModel em,
                               double thr, unsigned long long* rb_d, int* rb_j, double* rowlow,
                               int* amb, unsigned long long* amb_count,
-                              const int* __restrict__ orig) {
+                              const int* __restrict__ orig, int keys_lower) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   unsigned long long k1 = B1[i];
@@ -210,10 +210,12 @@ __global__ void refine_kernel(const double* __restrict__ X64, int n, int d,
   }
   int j = (int)key_index(k1);
   double e = exact_dist<M>(X64 + (int64_t)i * d, X64 + (int64_t)j * d, d);
+  // keys are screened values (direct form) or already rigorous lower bounds (dot form)
   double R = norm[i] + maxnorm;
-  rowlow[i] = exact_lower(em, (double)key_value(k1), R);
+  rowlow[i] = keys_lower ? (double)key_value(k1) : exact_lower(em, (double)key_value(k1), R);
   unsigned long long k2 = B2[i];
-  double low2 = key_valid(k2) ? exact_lower(em, (double)key_value(k2), R) : INFINITY;
+  double low2 = !key_valid(k2) ? INFINITY
+                : (keys_lower ? (double)key_value(k2) : exact_lower(em, (double)key_value(k2), R));
   if (e <= thr) {
     rb_d[i] = dbits(e);
     rb_j[i] = orig[j];  // partner as ORIGINAL index (tie-break order of the reference)
@@ -426,6 +428,44 @@ __global__ void tile_geom_kernel(const double* __restrict__ X64, const int* __re
     r = fmax(fmax(sr[0], sr[1]), fmax(sr[2], sr[3]));
     radius[T0] = r * (1.0 + 1e-9) + 1e-300;
   }
+}
+
+// dot-form constants per position of the Boruvka view (nnm_common.cuh DotModel)
+__global__ void dot_consts_kernel(const float* __restrict__ X32p, int64_t np, int d,
+                                  const int* __restrict__ porig, const double* __restrict__ tcenter,
+                                  const double* __restrict__ normp, double maxnorm, DotModel m,
+                                  float* __restrict__ c32, float* __restrict__ Bout,
+                                  float* __restrict__ nbk) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const int64_t T0 = p / TILE;
+  if (p % TILE == 0)
+    for (int k = 0; k < d; ++k) c32[T0 * d + k] = __double2float_rn(tcenter[T0 * d + k]);
+  if (porig[p] < 0) {
+    Bout[p] = 0.f;
+    nbk[p] = 0.f;
+    return;
+  }
+  double r2 = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const float c = __double2float_rn(tcenter[T0 * d + k]);
+    const float xh = X32p[(int64_t)k * np + p] - c;  // exactly what the kernel computes
+    r2 += (double)xh * (double)xh;
+  }
+  const double r = sqrt(r2) * (1.0 + 1e-12);
+  const double nb = dot_negB(m, r, normp[p], maxnorm);
+  nbk[p] = float_down(nb);
+  Bout[p] = float_up(-nb * (1.0 + m.A));
+}
+
+__global__ void tile_bmax_kernel(const float* __restrict__ B, float* __restrict__ bmax) {
+  const int T0 = blockIdx.x;
+  float v = B[(int64_t)T0 * TILE + threadIdx.x];
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  __shared__ float sm[4];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) bmax[T0] = fmaxf(fmaxf(sm[0], sm[1]), fmaxf(sm[2], sm[3]));
 }
 
 // lower bound on the exact internal value of every pair of tile pair (I, J)
@@ -1009,6 +1049,10 @@ struct nnm_dataset {
   int64_t vn = 0, vld = 0;
   int vT = 0;
   const int* cur_tcount = nullptr;
+  // dot form
+  bool dot_on = false;
+  DotModel dm{};
+  DevBuf<float> tcenter32, dotB, dotNBK, dotBmax;
   // pruning
   int geom_metric = -1;
   DevBuf<double> tcenter, tradius, tumax;
@@ -1134,6 +1178,17 @@ struct nnm_dataset {
     a.items = items;
     a.B1 = b1;
     a.B2 = b2;
+    a.dot_center = nullptr;
+    a.dot_B = a.dot_nbk = a.dot_Bmax = nullptr;
+    a.dot_k = a.dot_onepA = 1.f;
+    if (dot_on && cur_X32 == X32p.p) {
+      a.dot_center = tcenter32.p;
+      a.dot_B = dotB.p;
+      a.dot_nbk = dotNBK.p;
+      a.dot_Bmax = dotBmax.p;
+      a.dot_k = float_down(1.0 / (1.0 + dm.A));
+      a.dot_onepA = float_up(1.0 + dm.A);
+    }
     int occ = scan_occupancy(metric, d);
     int64_t nitems = w_end - w_begin;
     int grid = (int)std::min<int64_t>(nitems, (int64_t)sms * occ);
@@ -1240,9 +1295,14 @@ struct nnm_dataset {
     em = make_err_model(metric, d);
     bv_thr = INFINITY;
     bv_thr_hi = INFINITY;
+    ensure_geometry(metric);
+    const char* de = getenv("NNM_DOT");
+    dot_on = (metric == EUCLIDEAN || metric == SQEUCLIDEAN) && (de && de[0] == '1') &&
+             scan_use_ws(d);
     if (!std::isnan(dmax)) {
       bv_thr = metric == EUCLIDEAN ? dmax * dmax : dmax;  // metrics.py:93-103
-      bv_thr_hi = float_up(screen_upper(em, bv_thr, 2.0 * maxnorm));
+      // dot-form keys are lower bounds of S: compare them with thr itself
+      bv_thr_hi = dot_on ? float_up(bv_thr) : float_up(screen_upper(em, bv_thr, 2.0 * maxnorm));
     }
     comp.ensure(vn);
     fill_comp_view_kernel<<<blocks_for(vn), 256, 0, st>>>(porig.p, vn, comp.p); note_launch();
@@ -1373,6 +1433,17 @@ struct nnm_dataset {
     }
     note_launch();
     CUDA_TRY(cudaGetLastError());
+    if (kind == EUCLIDEAN) {
+      dm = make_dot_model(d);
+      tcenter32.ensure((size_t)Tp * d);
+      dotB.ensure(np_);
+      dotNBK.ensure(np_);
+      dotBmax.ensure(Tp);
+      dot_consts_kernel<<<blocks_for(np_), 256, 0, st>>>(X32p.p, np_, d, porig.p, tcenter.p, normp.p,
+                                                         maxnormp, dm, tcenter32.p, dotB.p, dotNBK.p); note_launch();
+      tile_bmax_kernel<<<Tp, TILE, 0, st>>>(dotB.p, dotBmax.p); note_launch();
+      CUDA_TRY(cudaGetLastError());
+    }
     geom_metric = kind;
   }
 
@@ -1496,7 +1567,7 @@ struct nnm_dataset {
   void refine_t(const unsigned long long* b1, const unsigned long long* b2) {
     refine_kernel<M><<<blocks_for(vn), 256, 0, st>>>(X64p.p, (int)vn, d, b1, b2, normp.p, maxnormp, em,
                                                     bv_thr, rb_d.p, rb_j.p, rowlow.p, amb.p,
-                                                    counters.p + 1, porig.p); note_launch();
+                                                    counters.p + 1, porig.p, dot_on ? 1 : 0); note_launch();
   }
 
   int64_t bv_finish_round(const unsigned long long* b1, const unsigned long long* b2) {
@@ -1629,6 +1700,7 @@ struct nnm_dataset {
   void top_p(int metric, double thr, int kl2, int kl3, int64_t P, std::vector<Cand>& out) {
     ensure_norms(metric);
     use_original_view();
+    dot_on = false;
     em = make_err_model(metric, d);
     float thr_hi = std::isinf(thr) ? INFINITY : float_up(screen_upper(em, thr, 2.0 * maxnorm));
     B1.ensure(n);

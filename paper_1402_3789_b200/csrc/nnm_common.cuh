@@ -124,11 +124,58 @@ __host__ __device__ inline double exact_lower(const ErrModel& e, double v, doubl
   return lo > 0.0 ? lo * (1.0 - 1e-12) : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Dot-form screen (Euclidean Boruvka scans).
+// For a tile pair (I, J) the kernel centres both tiles on c = fl32(centre of I):
+//   xh = fl(x32 - c), yh = fl(y32 - c),  v = fl(fl(|xh|^2 + |yh|^2) - 2 fl(xh.yh))
+// with FFMA accumulation.  With r = |xh| of the tile-I point and
+// eta0 = u(|x| + |y|max) + 2u(1+u) r  (input rounding + centring rounding):
+//   |v - S| <= A*S + B(r),  A = 2*alpha*(1+u)^2 + eps + 2u + 2u^2,
+//   B(r)    = 2*alpha*(2r + eta0)^2 + eta0^2 (1/eps + 2),  alpha = 1.1 (d+3) u
+// (triangle inequality on |xh - yh| vs sqrt(S), then (a+b)^2 <= 2a^2 + 2b^2 and
+// 2 sqrt(S) eta <= eps S + eta^2 / eps).  Keys store L = (v - B) / (1 + A)
+// rounded down, a rigorous LOWER bound of S.
+// ---------------------------------------------------------------------------
+struct DotModel {
+  double A;
+  double eps;
+  double alpha;
+  double u;
+};
+
+__host__ __device__ inline DotModel make_dot_model(int d) {
+  DotModel m;
+  m.u = 5.9604644775390625e-08;
+  m.alpha = 1.1 * (d + 3) * m.u;
+  m.eps = 1e-5;
+  m.A = 2.0 * m.alpha * (1 + m.u) * (1 + m.u) + m.eps + 2 * m.u + 2 * m.u * m.u;
+  m.A *= 1.01;
+  return m;
+}
+
+// per-point constant B (returned already multiplied by -1/(1+A), for one FFMA)
+__host__ __device__ inline double dot_negB(const DotModel& m, double r, double xnorm,
+                                           double maxnorm) {
+  double eta0 = m.u * (xnorm + maxnorm) * 1.01 + 2.0 * m.u * (1 + m.u) * r * 1.01;
+  double t = 2 * r + eta0;
+  double B = (2 * m.alpha * t * t + eta0 * eta0 * (1.0 / m.eps + 2.0)) * 1.01 + 1e-30;
+  return -B / (1.0 + m.A);
+}
+
 // float rounded toward +inf from a double (so float(v) >= v)
 __host__ __device__ inline float float_up(double v) {
   if (!(v < 3.0e38)) return INFINITY;
   float f = (float)v;
   if ((double)f < v) f = nextafterf(f, INFINITY);
+  return f;
+}
+
+// float rounded toward -inf from a double (so float(v) <= v)
+__host__ __device__ inline float float_down(double v) {
+  if (!(v > -3.0e38)) return -INFINITY;
+  if (!(v < 3.0e38)) return 3.0e38f;
+  float f = (float)v;
+  if ((double)f > v) f = nextafterf(f, -INFINITY);
   return f;
 }
 

@@ -22,6 +22,13 @@ struct ScanArgs {
   const int2* items;       // nullptr: item w = w-th upper-triangular tile pair; else items[w]
   unsigned long long* B1;  // [n] best screened key per row
   unsigned long long* B2;  // [n] second-best (TOP2 only)
+  // dot form (Euclidean Boruvka): keys are rigorous lower bounds L of S
+  const float* dot_center;  // [T][d] fl32 tile centres (nullptr: direct form)
+  const float* dot_B;       // [n] per-position B, rounded up
+  const float* dot_nbk;     // [n] -B/(1+A), rounded down
+  const float* dot_Bmax;    // [T] max B over the tile, rounded up
+  float dot_k;              // 1/(1+A) rounded down
+  float dot_onepA;          // 1+A rounded up
 };
 
 struct CollectArgs {

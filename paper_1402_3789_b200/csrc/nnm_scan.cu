@@ -158,6 +158,57 @@ __device__ __forceinline__ void tile_8x8(const float* __restrict__ sX, const flo
   }
 }
 
+// dot form: acc += yh * xh (one FFMA2 per two pairs and coordinate)
+__device__ __forceinline__ void dot_step(float2 (&acc)[8][4], float4 xa, float4 xb, float4 ya,
+                                         float4 yb) {
+  const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+  const float2 yc[4] = {make_float2(ya.x, ya.y), make_float2(ya.z, ya.w), make_float2(yb.x, yb.y),
+                        make_float2(yb.z, yb.w)};
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[r][q] = __ffma2_rn(yc[q], make_float2(xr[r], xr[r]), acc[r][q]);
+}
+
+__device__ __forceinline__ void tile_dot_8x8(const float* __restrict__ sX,
+                                             const float* __restrict__ sY, int d, int row0,
+                                             int colw, int tc, float2 (&acc)[8][4]) {
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[r][q] = make_float2(0.f, 0.f);
+  const float* __restrict__ xp = sX + row0;
+  const float* __restrict__ yp = sY + colw + tc * 4;
+  float4 a0 = *reinterpret_cast<const float4*>(xp), a1 = *reinterpret_cast<const float4*>(xp + 4);
+  float4 a2 = *reinterpret_cast<const float4*>(yp), a3 = *reinterpret_cast<const float4*>(yp + 32);
+  int k = 0;
+#pragma unroll 1
+  for (; k + 2 < d; k += 2) {
+    const float4 b0 = *reinterpret_cast<const float4*>(xp + TILE);
+    const float4 b1 = *reinterpret_cast<const float4*>(xp + TILE + 4);
+    const float4 b2 = *reinterpret_cast<const float4*>(yp + TILE);
+    const float4 b3 = *reinterpret_cast<const float4*>(yp + TILE + 32);
+    dot_step(acc, a0, a1, a2, a3);
+    xp += 2 * TILE;
+    yp += 2 * TILE;
+    a0 = *reinterpret_cast<const float4*>(xp);
+    a1 = *reinterpret_cast<const float4*>(xp + 4);
+    a2 = *reinterpret_cast<const float4*>(yp);
+    a3 = *reinterpret_cast<const float4*>(yp + 32);
+    dot_step(acc, b0, b1, b2, b3);
+  }
+  if (k + 1 < d) {
+    const float4 b0 = *reinterpret_cast<const float4*>(xp + TILE);
+    const float4 b1 = *reinterpret_cast<const float4*>(xp + TILE + 4);
+    const float4 b2 = *reinterpret_cast<const float4*>(yp + TILE);
+    const float4 b3 = *reinterpret_cast<const float4*>(yp + TILE + 32);
+    dot_step(acc, a0, a1, a2, a3);
+    dot_step(acc, b0, b1, b2, b3);
+  } else {
+    dot_step(acc, a0, a1, a2, a3);
+  }
+}
+
 __device__ __forceinline__ float acc_at(const float2 (&acc)[8][4], int r, int c) {
   return (c & 1) ? acc[r][c >> 1].y : acc[r][c >> 1].x;
 }
@@ -482,7 +533,7 @@ __device__ __forceinline__ unsigned long long widen(uint32_t k, unsigned long lo
                                   : (((unsigned long long)(k & ~63u) << 32) | (base + (k & 63u)));
 }
 
-template <int M, bool TOP2, bool SIZES, bool THR>
+template <int M, bool TOP2, bool SIZES, bool THR, bool DOT>
 __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int dT = p.d * TILE;
@@ -493,6 +544,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
   int* sCC = sCR + 2 * TILE;                        // [2][128] col comps
   int* sSR = sCC + 2 * TILE;                        // [2][128] row eff sizes
   int* sSC = sSR + 2 * TILE;                        // [2][128] col eff sizes
+  float* sNB = reinterpret_cast<float*>(sSC + 2 * TILE);  // [2][128] row -B/(1+A) (dot)
+  float* sNX = sNB + 2 * TILE;                            // [2 xb][2 halves][128] row norms
+  float* sNY = sNX + 4 * TILE;                            // [2 buf][2 halves][128] col norms
 
   const int64_t total = p.w_end - p.w_begin;
   const int64_t per = (total + gridDim.x - 1) / gridDim.x;
@@ -521,12 +575,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
       cp_async_commit();
     }
     int xb = 0;
+    bool xfresh = true;
     for (int64_t w = w0; w < w1; ++w) {
       const int buf = (int)((w - w0) & 1);
       int In, Jn;
       next_item(p, w, I, J, In, Jn);
       cp_async_wait_all();
       bar_sync(1, WS_COMPUTE_THREADS);  // tiles for w resident; everyone done with w-1
+      const bool xnew = xfresh;  // the row tile in sX[xb] still holds raw coordinates
+      xfresh = false;
       if (w + 1 < w1) {
         // this thread copies 16-byte column chunk (tid & 31) of rows k = tid/32 + 8i
         float* ny = sY0 + (buf ^ 1) * dT + (tid >> 5) * TILE + (tid & 31) * 4;
@@ -545,8 +602,56 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
         }
         cp_async_commit();
       }
+      if (DOT) {
+        // centre both tiles on c_I: yh = y - c_I (and xh when I is new), plus
+        // half-norms; thread t owns column / row (t & 127), coordinate half t >> 7
+        const int col = tid & (TILE - 1), hk = tid >> 7;
+        const int dh = (p.d + 1) >> 1, k0 = hk * dh, k1 = min(p.d, k0 + dh);
+        const float* cI = p.dot_center + (int64_t)I * p.d;
+        float* yb = sY0 + buf * dT;
+        float ny = 0.f;
+        for (int k = k0; k < k1; ++k) {
+          const float v = yb[k * TILE + col] - __ldg(cI + k);
+          yb[k * TILE + col] = v;
+          ny = fmaf(v, v, ny);
+        }
+        sNY[(buf * 2 + hk) * TILE + col] = ny;
+        if (w == w0 || xnew) {
+          float* xbuf = sX0 + xb * dT;
+          float nx = 0.f;
+          for (int k = k0; k < k1; ++k) {
+            const float v = xbuf[k * TILE + col] - __ldg(cI + k);
+            xbuf[k * TILE + col] = v;
+            nx = fmaf(v, v, nx);
+          }
+          sNX[(xb * 2 + hk) * TILE + col] = nx;
+        }
+        bar_sync(1, WS_COMPUTE_THREADS);
+      }
       float2 acc[8][4];
-      tile_8x8<M>(sX0 + xb * dT, sY0 + buf * dT, p.d, row0, colw, tc, acc);
+      if (DOT) tile_dot_8x8(sX0 + xb * dT, sY0 + buf * dT, p.d, row0, colw, tc, acc);
+      else tile_8x8<M>(sX0 + xb * dT, sY0 + buf * dT, p.d, row0, colw, tc, acc);
+      if (DOT) {
+        // v = |xh|^2 + |yh|^2 - 2 xh.yh
+        const float* nx0 = sNX + (xb * 2) * TILE;
+        const float* ny0 = sNY + (buf * 2) * TILE;
+        float nxr[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) nxr[r] = nx0[row0 + r] + nx0[TILE + row0 + r];
+        float2 nyc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c0 = colw + wcol(tc, 2 * q);
+          nyc[q] = make_float2(ny0[c0] + ny0[TILE + c0], ny0[c0 + 1] + ny0[TILE + c0 + 1]);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 s2 = __fadd2_rn(nyc[q], make_float2(nxr[r], nxr[r]));
+            acc[r][q] = __ffma2_rn(acc[r][q], make_float2(-2.f, -2.f), s2);
+          }
+      }
       bar_sync(4 + buf, WS_THREADS);  // EMPTY[buf]
       // element (R, 4q..4q+3) -> R*128 + ((q ^ (R & 31)) << 2); with R = row0 + r and
       // q = (wc*2 + h)*8 + tc the XOR splits into ((wc*2+h) ^ tr) << 5 | (tc ^ r) << 2
@@ -563,7 +668,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
         }
       }
       bar_arrive(2 + buf, WS_THREADS);  // FULL[buf]
-      if (In != I) xb ^= 1;
+      if (In != I) {
+        xb ^= 1;
+        xfresh = true;
+      }
       I = In;
       J = Jn;
     }
@@ -578,17 +686,24 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
     unsigned long long run1 = NONE_KEY, run2 = NONE_KEY;  // row t running top-2 over J
     bar_arrive(4, WS_THREADS);  // both distance buffers start empty
     bar_arrive(5, WS_THREADS);
+    // raw-value threshold equivalent to a key d-part: values (as signed ints, DOT
+    // values may be slightly negative) above it cannot produce a key <= d-part
+    auto vthr = [&](uint32_t dpart, float B) -> int {
+      const uint32_t tb = dpart | 63u;
+      if (!DOT) return (int)min(tb, 0x7FFFFFFFu);
+      if (tb >= INF_BITS) return 0x7FFFFFFF;
+      return __float_as_int(__fmaf_ru(__uint_as_float(tb), p.dot_onepA, B));
+    };
     for (int64_t w = w0; w < w1; ++w) {
       const int buf = (int)((w - w0) & 1);
       int In, Jn;
       next_item(p, w, I, J, In, Jn);
       const bool diag = (I == J);
-      const int2 rI = __ldg(p.tile_range + I), rJ = __ldg(p.tile_range + J);
-      const bool may_share = diag || !(rI.y < rJ.x || rJ.y < rI.x);
       int* cr = sCR + buf * TILE;
       int* cc = sCC + buf * TILE;
       int* sr = sSR + buf * TILE;
       int* sc = sSC + buf * TILE;
+      float* nb = sNB + buf * TILE;
       // my own label / size, and publish it for the other role
       const int mytile = is_row ? I : J;
       const int myC = __ldg(p.comp + (int64_t)mytile * TILE + t);
@@ -598,9 +713,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
         myS = __ldg(p.psize + (int64_t)mytile * TILE + t);
         (is_row ? sr : sc)[t] = myS;
       }
+      float myB = 0.f, myNBK = 0.f;
+      if (DOT && is_row) {
+        myB = __ldg(p.dot_B + (int64_t)I * TILE + t);
+        myNBK = __ldg(p.dot_nbk + (int64_t)I * TILE + t);
+        nb[t] = myNBK;
+      }
       // global second-best (best for top-1) d-parts: stale values are larger,
       // hence still safe filter thresholds
-      uint32_t growG = 0xFFFFFFFFu, gcolG = 0xFFFFFFFFu;
+      uint32_t growG = 0x7FFFFFFFu, gcolG = 0x7FFFFFFFu;
       {
         const unsigned long long* G = TOP2 ? p.B2 : p.B1;
         const int g = (is_row ? I : J) * TILE + t;
@@ -610,14 +731,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
           else gcolG = v;
         }
       }
+      const float colB = (DOT && !is_row) ? __ldg(p.dot_Bmax + I) : 0.f;
       bar_sync(6, WS_EPI_THREADS);
       bar_sync(2 + buf, WS_THREADS);  // FULL[buf]
       const float* D = sD + buf * TILE * TILE;
       unsigned long long k1 = NONE_KEY, k2 = NONE_KEY;
-      // Filter: a value whose masked d-part exceeds the d-part of a key already
-      // known to survive (running / global second-best; best for top-1) cannot
-      // enter the final top-2, so whole 4-value chunks are skipped with one
-      // warp vote.  Skipped values would only have produced larger keys.
+      // Filter: a value that cannot produce a key below a key already known to
+      // survive (running / global second-best; best for top-1) cannot enter the
+      // final top-2, so whole 4-value chunks are skipped with one warp vote.
       if (is_row) {
         const int tt = t & 31;
         const float* Drow = D + t * TILE;
@@ -626,18 +747,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
-          uint32_t thr = gthr | 63u;
+          int thr = vthr(gthr, myB);
 #pragma unroll 4
           for (int qq = 0; qq < 16; ++qq) {
             // logical chunk q sits at position q ^ tt: distinct positions across
             // the warp keep the LDS.128 bank-conflict free
             const int q = h * 16 + qq;
             const float4 v4 = *reinterpret_cast<const float4*>(Drow + ((q ^ tt) << 2));
-            const uint32_t b0 = __float_as_uint(v4.x), b1 = __float_as_uint(v4.y);
-            const uint32_t b2 = __float_as_uint(v4.z), b3 = __float_as_uint(v4.w);
-            const uint32_t mn = min(umin3(b0, b1, b2), b3);
+            const int mn = min(min(__float_as_int(v4.x), __float_as_int(v4.y)),
+                               min(__float_as_int(v4.z), __float_as_int(v4.w)));
             if (__any_sync(0xFFFFFFFFu, mn <= thr)) {
-              const uint32_t bb[4] = {b0, b1, b2, b3};
+              const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
               int4 s4 = make_int4(0, 0, 0, 0);
               const int4 c4 = *reinterpret_cast<const int4*>(cc + q * 4);
               if (SIZES) s4 = *reinterpret_cast<const int4*>(sc + q * 4);
@@ -647,19 +767,22 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
               uint32_t kk[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                bool ok = ca[e] != myC;
+                const float L = DOT ? fmaxf(__fmaf_rd(vv[e], p.dot_k, myNBK), 0.f) : vv[e];
+                // pads (label -1, +inf coordinates) never pair: in the dot form their
+                // values are inf / NaN, which fmaxf would turn into 0
+                bool ok = ca[e] != myC && ca[e] >= 0 && myC >= 0 && fabsf(vv[e]) < INFINITY;
                 if (SIZES) ok = ok && (myS + sa[e] <= p.ksum);
-                if (THR) ok = ok && (__uint_as_float(bb[e]) <= p.thr_hi);
-                const uint32_t bits = ok ? bb[e] : INF_BITS;
+                if (THR) ok = ok && (L <= p.thr_hi);
+                const uint32_t bits = ok ? __float_as_uint(L) : INF_BITS;
                 kk[e] = (bits & ~63u) | (cb + e);
               }
               if (TOP2) {
                 top2_pair(m1, m2, kk[0], kk[1]);
                 top2_pair(m1, m2, kk[2], kk[3]);
-                thr = min(gthr, m2 & ~63u) | 63u;
+                thr = vthr(min(gthr, m2 & ~63u), myB);
               } else {
                 m1 = min(min(m1, kk[0]), min(min(kk[1], kk[2]), kk[3]));
-                thr = min(gthr, m1 & ~63u) | 63u;
+                thr = vthr(min(gthr, m1 & ~63u), myB);
               }
             }
           }
@@ -676,39 +799,44 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu;
-          uint32_t thr = gthr | 63u;
+          int thr = vthr(gthr, colB);
 #pragma unroll
           for (int r4 = h * 16; r4 < h * 16 + 16; ++r4) {
-            uint32_t bb[4];
+            float vv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int r = r4 * 4 + u;
-              bb[u] = __float_as_uint(D[r * TILE + off[r & 31]]);
+              vv[u] = D[r * TILE + off[r & 31]];
             }
-            const uint32_t mn = min(umin3(bb[0], bb[1], bb[2]), bb[3]);
+            const int mn = min(min(__float_as_int(vv[0]), __float_as_int(vv[1])),
+                               min(__float_as_int(vv[2]), __float_as_int(vv[3])));
             if (__any_sync(0xFFFFFFFFu, mn <= thr)) {
               int4 s4 = make_int4(0, 0, 0, 0);
               const int4 c4 = *reinterpret_cast<const int4*>(cr + r4 * 4);
               if (SIZES) s4 = *reinterpret_cast<const int4*>(sr + r4 * 4);
+              float4 n4 = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (DOT) n4 = *reinterpret_cast<const float4*>(nb + r4 * 4);
               const int ca[4] = {c4.x, c4.y, c4.z, c4.w};
               const int sa[4] = {s4.x, s4.y, s4.z, s4.w};
+              const float na[4] = {n4.x, n4.y, n4.z, n4.w};
               uint32_t kk[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int r = r4 * 4 + u;
-                bool ok = ca[u] != myC;
+                const float L = DOT ? fmaxf(__fmaf_rd(vv[u], p.dot_k, na[u]), 0.f) : vv[u];
+                bool ok = ca[u] != myC && ca[u] >= 0 && myC >= 0 && fabsf(vv[u]) < INFINITY;
                 if (SIZES) ok = ok && (myS + sa[u] <= p.ksum);
-                if (THR) ok = ok && (__uint_as_float(bb[u]) <= p.thr_hi);
-                const uint32_t bits = ok ? bb[u] : INF_BITS;
+                if (THR) ok = ok && (L <= p.thr_hi);
+                const uint32_t bits = ok ? __float_as_uint(L) : INF_BITS;
                 kk[u] = (bits & ~63u) | (uint32_t)(r & 63);
               }
               if (TOP2) {
                 top2_pair(m1, m2, kk[0], kk[1]);
                 top2_pair(m1, m2, kk[2], kk[3]);
-                thr = min(gthr, m2 & ~63u) | 63u;
+                thr = vthr(min(gthr, m2 & ~63u), colB);
               } else {
                 m1 = min(min(m1, kk[0]), min(min(kk[1], kk[2]), kk[3]));
-                thr = min(gthr, m1 & ~63u) | 63u;
+                thr = vthr(min(gthr, m1 & ~63u), colB);
               }
             }
           }
@@ -737,14 +865,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
 
 size_t scan_ws_smem_bytes(int d) {
   return (size_t)2 * TILE * TILE * sizeof(float) + (size_t)4 * d * TILE * sizeof(float) +
-         8 * TILE * sizeof(int);
+         8 * TILE * sizeof(int) + (2 + 4 + 4) * TILE * sizeof(float);
 }
 
 template <int M, bool TOP2, bool SIZES, bool THR>
 static cudaError_t launch_scan_t(const ScanArgs& a, int grid, cudaStream_t st) {
   if (scan_use_ws(a.d)) {
     size_t sm = scan_ws_smem_bytes(a.d);
-    auto k = scan_ws_kernel<M, TOP2, SIZES, THR>;
+    auto k = (M == EUCLIDEAN && a.dot_center) ? scan_ws_kernel<M, TOP2, SIZES, THR, true>
+                                              : scan_ws_kernel<M, TOP2, SIZES, THR, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     k<<<grid, WS_THREADS, sm, st>>>(a);
