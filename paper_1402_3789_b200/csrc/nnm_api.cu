@@ -1189,7 +1189,7 @@ struct nnm_dataset {
       a.dot_k = float_down(1.0 / (1.0 + dm.A));
       a.dot_onepA = float_up(1.0 + dm.A);
     }
-    int occ = scan_occupancy(metric, d);
+    int occ = scan_use_reg(a) ? 2 : scan_occupancy(metric, d);
     int64_t nitems = w_end - w_begin;
     int grid = (int)std::min<int64_t>(nitems, (int64_t)sms * occ);
     if (grid < 1) return;
@@ -1297,7 +1297,7 @@ struct nnm_dataset {
     bv_thr_hi = INFINITY;
     ensure_geometry(metric);
     const char* de = getenv("NNM_DOT");
-    dot_on = (metric == EUCLIDEAN || metric == SQEUCLIDEAN) && (de && de[0] == '1') &&
+    dot_on = (metric == EUCLIDEAN || metric == SQEUCLIDEAN) && !(de && de[0] == '0') &&
              scan_use_ws(d);
     if (!std::isnan(dmax)) {
       bv_thr = metric == EUCLIDEAN ? dmax * dmax : dmax;  // metrics.py:93-103

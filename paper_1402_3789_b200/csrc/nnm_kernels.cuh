@@ -55,6 +55,8 @@ size_t scan_smem_bytes(int d);
 size_t collect_smem_bytes(int d);
 int scan_occupancy(int metric, int d);
 bool scan_use_ws(int d);
+bool scan_use_reg(const ScanArgs& a);
+size_t scan_reg_smem_bytes(int d);
 size_t scan_ws_smem_bytes(int d);
 void scan_set_mode(int mode);  // -1 auto, 0 classic kernel, 1 warp-specialised
 cudaError_t launch_scan(int metric, const ScanArgs& a, bool top2, int grid, cudaStream_t st);

@@ -484,8 +484,19 @@ bool scan_use_ws(int d) {
 
 void scan_set_mode(int mode) { g_ws_mode = mode; }
 
+// register-epilogue kernel: the default for Boruvka (top-2) scans
+bool scan_use_reg(const ScanArgs& a) {
+  if (scan_reg_smem_bytes(a.d) > 110 * 1024) return false;
+  const char* e = getenv("NNM_SCAN_KERNEL");
+  if (e && e[0] == 'r') return true;
+  if (e && (e[0] == 'w' || e[0] == 'c')) return false;
+  // top-2 (Boruvka) scans: the filter thresholds come from second-best keys
+  // that fill quickly; top-1 round scans (fresh B1 every round) stay on WS
+  return a.B2 != nullptr;
+}
+
 int scan_occupancy(int metric, int d) {
-  if (scan_use_ws(d)) return 1;
+  if (scan_use_ws(d)) return 1;  // (the register kernel also runs 2 CTAs / SM: see launch)
   int blocks = 0;
   size_t sm = scan_smem_bytes(d);
   cudaFuncSetAttribute(scan_rows_kernel<EUCLIDEAN, true, false, false>,
@@ -868,8 +879,260 @@ size_t scan_ws_smem_bytes(int d) {
          8 * TILE * sizeof(int) + (2 + 4 + 4) * TILE * sizeof(float);
 }
 
+
+// ----------------------------------------------------------------------------
+// K1-REG: register-epilogue scan (default for the dot form).
+//
+// 2 CTAs / SM x 8 warps; a thread holds an 8x8 block of distances in registers.
+// Selection is a threshold filter: per row / column the kernel knows a key
+// already guaranteed to survive (running or global second-best); a value that
+// cannot beat it cannot enter the final top-2.  Thresholds are checked with a
+// few FMNMX per pair and one warp vote; the rare survivors are inserted exactly
+// (full 64-bit keys, no index truncation) into shared-memory top-2 slots with
+// atomics, flushed to global once per column tile / row tile.  No distance
+// tile ever touches shared memory.
+// ----------------------------------------------------------------------------
+template <int M, bool TOP2, bool SIZES, bool THR, bool DOT>
+__global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int dT = p.d * TILE;
+  unsigned long long* rowTop = reinterpret_cast<unsigned long long*>(smem_raw);  // [2 xb][2][128]
+  unsigned long long* colTop = rowTop + 4 * TILE;                               // [2 buf][2][128]
+  float* sX0 = reinterpret_cast<float*>(colTop + 4 * TILE);                    // [2][d*128]
+  float* sY0 = sX0 + 2 * dT;                                                    // [2][d*128]
+  float* sNX = sY0 + 2 * dT;   // [2 xb][2 halves][128]
+  float* sNY = sNX + 4 * TILE; // [2 buf][2 halves][128]
+  float* sBr = sNY + 4 * TILE; // [2 xb][128] row B (dot)
+  float* sNBr = sBr + 2 * TILE;  // [2 xb][128] row -B/(1+A) (dot)
+  int* sCR = reinterpret_cast<int*>(sNBr + 2 * TILE);  // [2 xb][128]
+  int* sCC = sCR + 2 * TILE;                            // [2 buf][128]
+  int* sSR = sCC + 2 * TILE;                            // [2 xb][128]
+  int* sSC = sSR + 2 * TILE;                            // [2 buf][128]
+  uint32_t* sGR = reinterpret_cast<uint32_t*>(sSC + 2 * TILE);  // [2 xb][128] global row d-parts
+  uint32_t* sGC = sGR + 2 * TILE;                               // [2 buf][128] global col d-parts
+
+  const int64_t total = p.w_end - p.w_begin;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = p.w_begin + (int64_t)blockIdx.x * per;
+  const int64_t w1 = min(w0 + per, p.w_end);
+  if (w0 >= w1) return;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wr = warp >> 1, wc = warp & 1;
+  const int tr = lane >> 3, tc = lane & 7;
+  const int row0 = wr * 32 + tr * 8;
+  const int colw = wc * 64;
+  const unsigned long long* Gsrc = TOP2 ? p.B2 : p.B1;
+
+  int I, J;
+  first_item(p, w0, I, J);
+  // prologue: row tile + labels, first column tile + labels
+  async_tile(sX0, sCR, sSR, p.X32, p.ld, I, p.d, p.comp, p.psize, SIZES);
+  async_tile(sY0, sCC, sSC, p.X32, p.ld, J, p.d, p.comp, p.psize, SIZES);
+  cp_async_commit();
+  for (int t = tid; t < 8 * TILE; t += SCAN_THREADS) rowTop[t] = NONE_KEY;  // rowTop + colTop
+  int xb = 0;
+  bool xfresh = true;
+  int prevI = -1, prevJ = -1, prevBuf = 0, prevXb = 0;
+  for (int64_t w = w0; w <= w1; ++w) {
+    const int buf = (int)((w - w0) & 1);
+    cp_async_wait_all();
+    __syncthreads();  // (A) tiles of w resident; inserts of w-1 complete
+    // ---- flush the previous item's column slots, and its row slots if I changes
+    if (prevJ >= 0) {
+      if (tid < TILE) {
+        if (prevI != prevJ) {
+          unsigned long long* ct = colTop + prevBuf * 2 * TILE;
+          const int g = prevJ * TILE + tid;
+          if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, ct[tid], ct[TILE + tid]);
+          ct[tid] = NONE_KEY;
+          ct[TILE + tid] = NONE_KEY;
+        }
+      } else if (w == w1 || I != prevI) {
+        const int r = tid - TILE;
+        unsigned long long* rt = rowTop + prevXb * 2 * TILE;
+        const int g = prevI * TILE + r;
+        if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, rt[r], rt[TILE + r]);
+        rt[r] = NONE_KEY;
+        rt[TILE + r] = NONE_KEY;
+      }
+    }
+    if (w == w1) break;
+    int In, Jn;
+    next_item(p, w, I, J, In, Jn);
+    const bool has_next = (w + 1 < w1);
+    if (has_next) {
+      async_tile(sY0 + (buf ^ 1) * dT, sCC + (buf ^ 1) * TILE, sSC + (buf ^ 1) * TILE, p.X32, p.ld,
+                 Jn, p.d, p.comp, p.psize, SIZES);
+      if (In != I)
+        async_tile(sX0 + (xb ^ 1) * dT, sCR + (xb ^ 1) * TILE, sSR + (xb ^ 1) * TILE, p.X32, p.ld,
+                   In, p.d, p.comp, p.psize, SIZES);
+      cp_async_commit();
+    }
+    float* sX = sX0 + xb * dT;
+    float* sY = sY0 + buf * dT;
+    // ---- per-tile setup: centring (dot form), global thresholds
+    {
+      const int col = tid & (TILE - 1), hk = tid >> 7;
+      if (DOT) {
+        const int dh = (p.d + 1) >> 1, k0 = hk * dh, k1 = min(p.d, k0 + dh);
+        const float* cI = p.dot_center + (int64_t)I * p.d;
+        float ny = 0.f;
+        for (int k = k0; k < k1; ++k) {
+          const float v = sY[k * TILE + col] - __ldg(cI + k);
+          sY[k * TILE + col] = v;
+          ny = fmaf(v, v, ny);
+        }
+        sNY[(buf * 2 + hk) * TILE + col] = ny;
+        if (xfresh) {
+          float nx = 0.f;
+          for (int k = k0; k < k1; ++k) {
+            const float v = sX[k * TILE + col] - __ldg(cI + k);
+            sX[k * TILE + col] = v;
+            nx = fmaf(v, v, nx);
+          }
+          sNX[(xb * 2 + hk) * TILE + col] = nx;
+        }
+      }
+      if (hk == 0) {
+        const int g = J * TILE + col;
+        sGC[buf * TILE + col] = g < p.n ? (uint32_t)(*((volatile const unsigned long long*)(Gsrc + g)) >> 32)
+                                        : 0x7FFFFFFFu;
+      } else if (xfresh) {
+        const int g = I * TILE + col;
+        sGR[xb * TILE + col] = g < p.n ? (uint32_t)(*((volatile const unsigned long long*)(Gsrc + g)) >> 32)
+                                       : 0x7FFFFFFFu;
+        if (DOT) {
+          sBr[xb * TILE + col] = __ldg(p.dot_B + (int64_t)I * TILE + col);
+          sNBr[xb * TILE + col] = __ldg(p.dot_nbk + (int64_t)I * TILE + col);
+        }
+      }
+    }
+    xfresh = false;
+    __syncthreads();  // (B) centred tiles, norms, thresholds visible
+    float2 acc[8][4];
+    if (DOT) tile_dot_8x8(sX, sY, p.d, row0, colw, tc, acc);
+    else tile_8x8<M>(sX, sY, p.d, row0, colw, tc, acc);
+    float nbr[8];
+    if (DOT) {
+      const float* nx0 = sNX + (xb * 2) * TILE;
+      const float* ny0 = sNY + (buf * 2) * TILE;
+      float nxr[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        nxr[r] = nx0[row0 + r] + nx0[TILE + row0 + r];
+        nbr[r] = sNBr[xb * TILE + row0 + r];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c0 = colw + wcol(tc, 2 * q);
+        const float2 nyc = make_float2(ny0[c0] + ny0[TILE + c0], ny0[c0 + 1] + ny0[TILE + c0 + 1]);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float2 s2 = __fadd2_rn(nyc, make_float2(nxr[r], nxr[r]));
+          acc[r][q] = __ffma2_rn(acc[r][q], make_float2(-2.f, -2.f), s2);
+        }
+      }
+    }
+    // ---- thresholds in value units (pads: -inf, never pass)
+    const bool diag = (I == J);
+    const unsigned long long* rt = rowTop + xb * 2 * TILE;
+    unsigned long long* ct = colTop + buf * 2 * TILE;
+    float tR[8], tC[8];
+    const float bmax = DOT ? __ldg(p.dot_Bmax + I) : 0.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int R = row0 + t, C = colw + wcol(tc, t);
+      uint32_t dr = min(sGR[xb * TILE + R], (uint32_t)((TOP2 ? rt[TILE + R] : rt[R]) >> 32));
+      uint32_t dc = min(sGC[buf * TILE + C], (uint32_t)((TOP2 ? ct[TILE + C] : ct[C]) >> 32));
+      float fr = dr >= INF_BITS ? INFINITY : __uint_as_float(dr | 63u);
+      float fc = dc >= INF_BITS ? INFINITY : __uint_as_float(dc | 63u);
+      if (DOT) {
+        fr = __fmaf_ru(fr, p.dot_onepA, sBr[xb * TILE + R]);
+        fc = __fmaf_ru(fc, p.dot_onepA, bmax);
+      }
+      tR[t] = sCR[xb * TILE + R] >= 0 ? fr : -INFINITY;
+      tC[t] = sCC[buf * TILE + C] >= 0 ? fc : -INFINITY;
+    }
+    // ---- filter: any value at or below its row or column threshold?
+    bool hit = false;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float m = fminf(fminf(fminf(acc[r][0].x, acc[r][0].y), fminf(acc[r][1].x, acc[r][1].y)),
+                            fminf(fminf(acc[r][2].x, acc[r][2].y), fminf(acc[r][3].x, acc[r][3].y)));
+      hit |= m <= tR[r];
+    }
+    if (!diag) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float m = acc_at(acc, 0, c);
+#pragma unroll
+        for (int r = 1; r < 8; ++r) m = fminf(m, acc_at(acc, r, c));
+        hit |= m <= tC[c];
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, hit)) {
+      // rare exact path: insert every surviving pair into the shared top-2 slots
+      // (fully unrolled: dynamic indexing would move acc[] to local memory)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int R = row0 + r;
+        const int cR = sCR[xb * TILE + R];
+        const int sRv = SIZES ? sSR[xb * TILE + R] : 0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int C = colw + wcol(tc, c);
+          const float v = acc_at(acc, r, c);
+          const bool prow = v <= tR[r];
+          const bool pcol = !diag && v <= tC[c];
+          if (!(prow || pcol)) continue;
+          const int cC = sCC[buf * TILE + C];
+          bool ok = cR != cC && cR >= 0 && cC >= 0 && fabsf(v) < INFINITY;
+          if (SIZES) ok = ok && (sRv + sSC[buf * TILE + C] <= p.ksum);
+          const float L = DOT ? fmaxf(__fmaf_rd(v, p.dot_k, nbr[r]), 0.f) : v;
+          if (THR) ok = ok && (L <= p.thr_hi);
+          if (!ok) continue;
+          const unsigned long long dp = (unsigned long long)__float_as_uint(L) << 32;
+          if (prow)
+            insert_top2(const_cast<unsigned long long*>(rt) + R,
+                        TOP2 ? const_cast<unsigned long long*>(rt) + TILE + R : nullptr,
+                        dp | (unsigned long long)(J * TILE + C), NONE_KEY);
+          if (pcol)
+            insert_top2(ct + C, TOP2 ? ct + TILE + C : nullptr,
+                        dp | (unsigned long long)(I * TILE + R), NONE_KEY);
+        }
+      }
+    }
+    prevI = I;
+    prevJ = J;
+    prevBuf = buf;
+    prevXb = xb;
+    if (In != I) {
+      xb ^= 1;
+      xfresh = true;
+    }
+    I = In;
+    J = Jn;
+  }
+}
+
+size_t scan_reg_smem_bytes(int d) {
+  return (size_t)8 * TILE * sizeof(unsigned long long) + (size_t)4 * d * TILE * sizeof(float) +
+         (4 + 4 + 2 + 2) * TILE * sizeof(float) + 8 * TILE * sizeof(int) + 4 * TILE * sizeof(uint32_t);
+}
+
 template <int M, bool TOP2, bool SIZES, bool THR>
 static cudaError_t launch_scan_t(const ScanArgs& a, int grid, cudaStream_t st) {
+  if (scan_use_reg(a)) {
+    size_t sm = scan_reg_smem_bytes(a.d);
+    auto k = (M == EUCLIDEAN && a.dot_center) ? scan_reg_kernel<M, TOP2, SIZES, THR, true>
+                                              : scan_reg_kernel<M, TOP2, SIZES, THR, false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k<<<grid, SCAN_THREADS, sm, st>>>(a);
+    return cudaGetLastError();
+  }
   if (scan_use_ws(a.d)) {
     size_t sm = scan_ws_smem_bytes(a.d);
     auto k = (M == EUCLIDEAN && a.dot_center) ? scan_ws_kernel<M, TOP2, SIZES, THR, true>
