@@ -172,11 +172,14 @@ __device__ __forceinline__ void dot_step(float2 (&acc)[8][4], float4 xa, float4 
 
 __device__ __forceinline__ void tile_dot_8x8(const float* __restrict__ sX,
                                              const float* __restrict__ sY, int d, int row0,
-                                             int colw, int tc, float2 (&acc)[8][4]) {
+                                             int colw, int tc, float2 (&acc)[8][4],
+                                             bool zero = true) {
+  if (zero) {
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[r][q] = make_float2(0.f, 0.f);
+      for (int q = 0; q < 4; ++q) acc[r][q] = make_float2(0.f, 0.f);
+  }
   const float* __restrict__ xp = sX + row0;
   const float* __restrict__ yp = sY + colw + tc * 4;
   float4 a0 = *reinterpret_cast<const float4*>(xp), a1 = *reinterpret_cast<const float4*>(xp + 4);
@@ -1012,10 +1015,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
     xfresh = false;
     __syncthreads();  // (B) centred tiles, norms, thresholds visible
     float2 acc[8][4];
-    if (DOT) tile_dot_8x8(sX, sY, p.d, row0, colw, tc, acc);
-    else tile_8x8<M>(sX, sY, p.d, row0, colw, tc, acc);
     float nbr[8];
     if (DOT) {
+      // fold the norms into the accumulator start: acc = -(|xh|^2 + |yh|^2)/2 + xh.yh,
+      // so v = -2 acc needs no per-pair work after the loop
       const float* nx0 = sNX + (xb * 2) * TILE;
       const float* ny0 = sNY + (buf * 2) * TILE;
       float nxr[8];
@@ -1029,11 +1032,12 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
         const int c0 = colw + wcol(tc, 2 * q);
         const float2 nyc = make_float2(ny0[c0] + ny0[TILE + c0], ny0[c0 + 1] + ny0[TILE + c0 + 1]);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const float2 s2 = __fadd2_rn(nyc, make_float2(nxr[r], nxr[r]));
-          acc[r][q] = __ffma2_rn(acc[r][q], make_float2(-2.f, -2.f), s2);
-        }
+        for (int r = 0; r < 8; ++r)
+          acc[r][q] = __fmul2_rn(__fadd2_rn(nyc, make_float2(nxr[r], nxr[r])), make_float2(-0.5f, -0.5f));
       }
+      tile_dot_8x8(sX, sY, p.d, row0, colw, tc, acc, false);
+    } else {
+      tile_8x8<M>(sX, sY, p.d, row0, colw, tc, acc);
     }
     // ---- thresholds in value units (pads: -inf, never pass)
     const bool diag = (I == J);
@@ -1055,21 +1059,28 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
       tR[t] = sCR[xb * TILE + R] >= 0 ? fr : -INFINITY;
       tC[t] = sCC[buf * TILE + C] >= 0 ? fc : -INFINITY;
     }
-    // ---- filter: any value at or below its row or column threshold?
+    // ---- filter: any value at or below its row or column threshold?  (dot form:
+    // v = -2 acc, so v <= t  <=>  acc >= -t/2, an exact rescaling)
     bool hit = false;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
-      const float m = fminf(fminf(fminf(acc[r][0].x, acc[r][0].y), fminf(acc[r][1].x, acc[r][1].y)),
-                            fminf(fminf(acc[r][2].x, acc[r][2].y), fminf(acc[r][3].x, acc[r][3].y)));
-      hit |= m <= tR[r];
+      if (DOT) {
+        const float m = fmaxf(fmaxf(fmaxf(acc[r][0].x, acc[r][0].y), fmaxf(acc[r][1].x, acc[r][1].y)),
+                              fmaxf(fmaxf(acc[r][2].x, acc[r][2].y), fmaxf(acc[r][3].x, acc[r][3].y)));
+        hit |= m >= -0.5f * tR[r];
+      } else {
+        const float m = fminf(fminf(fminf(acc[r][0].x, acc[r][0].y), fminf(acc[r][1].x, acc[r][1].y)),
+                              fminf(fminf(acc[r][2].x, acc[r][2].y), fminf(acc[r][3].x, acc[r][3].y)));
+        hit |= m <= tR[r];
+      }
     }
     if (!diag) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         float m = acc_at(acc, 0, c);
 #pragma unroll
-        for (int r = 1; r < 8; ++r) m = fminf(m, acc_at(acc, r, c));
-        hit |= m <= tC[c];
+        for (int r = 1; r < 8; ++r) m = DOT ? fmaxf(m, acc_at(acc, r, c)) : fminf(m, acc_at(acc, r, c));
+        hit |= DOT ? (m >= -0.5f * tC[c]) : (m <= tC[c]);
       }
     }
     if (__any_sync(0xFFFFFFFFu, hit)) {
@@ -1083,7 +1094,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int C = colw + wcol(tc, c);
-          const float v = acc_at(acc, r, c);
+          const float v = DOT ? -2.f * acc_at(acc, r, c) : acc_at(acc, r, c);
           const bool prow = v <= tR[r];
           const bool pcol = !diag && v <= tC[c];
           if (!(prow || pcol)) continue;
