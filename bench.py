@@ -170,11 +170,13 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def _load_traffic():
+def _load_traffic_per_pair():
+    """DRAM bytes per evaluated pair of the scan kernel, from the committed ncu
+    capture (profiles/scan_traffic.json, one full dense launch)."""
     p = os.path.join(ROOT, "profiles", "scan_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            return json.load(open(p)).get("dram_bytes_per_pair")
         except (OSError, ValueError):
             return None
     return None
@@ -285,9 +287,14 @@ def run_gpu(args) -> None:
     # time of all scan launches (launch sizes differ once tile pairs are pruned)
     pairs_eval = sum(s["pairs_evaluated"] for s in stats)
     achieved = pairs_eval * 3 * d / (scan_ms / 1e3) / 1e12
+    bpp = _load_traffic_per_pair()
     roofline = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                "frac": achieved / peak.value if peak.value else None, "traffic": _load_traffic(),
-                "kernel": "scan_rows_kernel (fused FP32 distance + eligibility + per-row top-2)",
+                "frac": achieved / peak.value if peak.value else None,
+                "traffic": (bpp * pairs_eval / max(scans, 1)) if bpp is not None else None,
+                "traffic_note": "dram bytes per launch = ncu dram__bytes_read+write per pair "
+                                "(profiles/scan_traffic.json) x average pairs per launch",
+                "kernel": "scan_reg_kernel (fused FP32 dot-form distance + eligibility + per-row "
+                          "top-2 threshold filter)",
                 "peak_source": "measured FFMA2 microbenchmark on this GPU (MEASURED_PEAKS.json has no FP32 entry)",
                 "avg_launch_ms": avg_launch_ms, "launches": scans,
                 "scan_share_of_step": scan_ms / (ms_dev * args.steps)}
