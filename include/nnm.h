@@ -86,6 +86,9 @@ typedef struct {
   int64_t boruvka_rounds;
   int64_t kernel_launches; /* libnnm kernels launched by the call (library sorts excluded) */
   double pairs_covered;    /* pairs the rounds decided (evaluated or excluded by an exact bound) */
+  double prep_ms;          /* one-time per dataset/metric work done by this call (spatial view,
+                              norms, tile balls); 0 when cached */
+  double replay_ms;        /* edge sort + union-find replay into the merge log */
 } nnm_stats;
 
 int nnm_abi_version(void);

@@ -49,7 +49,8 @@ class Stats(ctypes.Structure):
                 ("pairs_evaluated", ctypes.c_double), ("scan_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("ambiguous_rows", ctypes.c_int64),
                 ("exact_evals", ctypes.c_int64), ("boruvka_rounds", ctypes.c_int64),
-                ("kernel_launches", ctypes.c_int64), ("pairs_covered", ctypes.c_double)]
+                ("kernel_launches", ctypes.c_int64), ("pairs_covered", ctypes.c_double),
+                ("prep_ms", ctypes.c_double), ("replay_ms", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

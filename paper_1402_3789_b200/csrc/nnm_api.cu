@@ -25,6 +25,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -70,23 +71,31 @@ int guarded(F&& f) {
   }
 }
 
+// Device buffers come from the stream-ordered pool (cudaMallocAsync) on the
+// stream of the dataset being worked on, with the pool's release threshold
+// raised: repeated dataset create / destroy (one per user call through the
+// reference-facing API) then costs no cudaMalloc / device-wide cudaFree syncs.
+thread_local cudaStream_t t_alloc_stream = nullptr;
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   }
   void ensure(size_t count) {
     if (count <= n && p) return;
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    s = t_alloc_stream;
     size_t c = count > 0 ? count : 1;
-    CUDA_TRY(cudaMalloc(&p, c * sizeof(T)));
+    CUDA_TRY(cudaMallocAsync((void**)&p, c * sizeof(T), s));
     n = c;
   }
 };
@@ -992,10 +1001,51 @@ __global__ void ones_kernel(int* a, int n) {
 
 }  // namespace nnm
 
+
+// Caching allocator for thrust temporaries: thrust would cudaMalloc / cudaFree
+// per call (cudaFree synchronises the device); blocks are reused per dataset.
+struct CachedAlloc {
+  typedef char value_type;
+  std::multimap<size_t, char*> free_blocks;
+  std::map<char*, size_t> used;
+  char* allocate(std::ptrdiff_t n) {
+    auto it = free_blocks.lower_bound((size_t)n);
+    if (it != free_blocks.end() && it->first <= 2 * (size_t)n + (1 << 20)) {
+      char* p = it->second;
+      used[p] = it->first;
+      free_blocks.erase(it);
+      return p;
+    }
+    char* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, (size_t)n));
+    used[p] = (size_t)n;
+    return p;
+  }
+  void deallocate(char* p, size_t) {
+    auto it = used.find(p);
+    free_blocks.emplace(it->second, p);
+    used.erase(it);
+  }
+  void release() {
+    for (auto& kv : free_blocks) cudaFree(kv.second);
+    for (auto& kv : used) cudaFree(kv.first);
+    free_blocks.clear();
+    used.clear();
+  }
+};
+
 // ----------------------------------------------------------------------------
 // dataset handle
 // ----------------------------------------------------------------------------
+struct StreamHolder {
+  cudaStream_t st = nullptr;
+  ~StreamHolder() {
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
 struct nnm_dataset {
+  StreamHolder stream_holder;  // declared first: destroyed after every DevBuf member
   std::mutex mu;
   int device = 0;
   int64_t n = 0;
@@ -1069,14 +1119,16 @@ struct nnm_dataset {
   DevBuf<int> active, rmap, rsize;
   DevBuf<int2> kv;
   nnm_stats stats{};
-  std::vector<float> scan_ms_pending;
+  CachedAlloc talloc;
 
   ~nnm_dataset() {
+    // members (DevBuf) free asynchronously on st after this body; the stream is
+    // destroyed last (cudaStreamDestroy defers until the queued frees finish)
     if (st) {
       cudaSetDevice(device);
       cudaStreamSynchronize(st);
-      cudaStreamDestroy(st);
     }
+    talloc.release();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
   }
@@ -1374,10 +1426,10 @@ struct nnm_dataset {
         cbase.ensure(nseg + 1);
         kd_dim_kernel<<<nseg, 32, 0, st>>>(X64.p, d, order.p, sbeg.p, ssz.p, nseg, sdim.p); note_launch();
         kd_key_kernel<<<blocks_for(n), 256, 0, st>>>(X64.p, n, d, order.p, segid.p, sdim.p, keys.p); note_launch();
-        thrust::stable_sort_by_key(thrust::cuda::par.on(st), keys.p, keys.p + n, order.p);
+        thrust::stable_sort_by_key(thrust::cuda::par(talloc).on(st), keys.p, keys.p + n, order.p);
         kd_splitpos_kernel<<<nseg, 32, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, ssplit.p); note_launch();
         kd_children_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, ssz.p, nchild.p); note_launch();
-        thrust::exclusive_scan(thrust::cuda::par.on(st), nchild.p, nchild.p + nseg, cbase.p, 0);
+        thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), nchild.p, nchild.p + nseg, cbase.p, 0);
         int lastc = read1(nchild.p + (nseg - 1)), lastb = read1(cbase.p + (nseg - 1));
         const int nseg2 = lastb + lastc;
         nbeg.ensure(nseg2);
@@ -1456,8 +1508,8 @@ struct nnm_dataset {
     CUDA_TRY(cudaGetLastError());
     auto* k64 = reinterpret_cast<unsigned long long*>(items1.p);  // (I, J) -> J << 32 | I order
     // sort by (I, J): int2 memory is {x=I, y=J}; as u64 little-endian = J << 32 | I -> swap to key
-    thrust::sort(thrust::cuda::par.on(st), k64, k64 + (size_t)Tp * PK, ItemLess());
-    auto* end = thrust::unique(thrust::cuda::par.on(st), k64, k64 + (size_t)Tp * PK);
+    thrust::sort(thrust::cuda::par(talloc).on(st), k64, k64 + (size_t)Tp * PK, ItemLess());
+    auto* end = thrust::unique(thrust::cuda::par(talloc).on(st), k64, k64 + (size_t)Tp * PK);
     n1 = end - k64;
     // drop the (-1,-1) padding, which sorts first
     int2 first = read1(items1.p);
@@ -1483,7 +1535,7 @@ struct nnm_dataset {
     enum_count_kernel<M><<<Tp, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, tumax.p, pbits.p, Tp, d,
                                              pkeep.p, pcount.p); note_launch();
     CUDA_TRY(cudaGetLastError());
-    thrust::exclusive_scan(thrust::cuda::par.on(st), pcount.p, pcount.p + Tp, poffset.p, 0LL);
+    thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), pcount.p, pcount.p + Tp, poffset.p, 0LL);
     long long last_off = read1(poffset.p + (Tp - 1));
     int last_cnt = read1(pcount.p + (Tp - 1));
     n2 = last_off + last_cnt;
@@ -1636,7 +1688,7 @@ struct nnm_dataset {
     unsigned long long ne = read1(counters.p);
     std::vector<Edge> h(ne);
     if (ne > 0) {
-      thrust::sort(thrust::cuda::par.on(st), edges.p, edges.p + ne, EdgeLess());
+      thrust::sort(thrust::cuda::par(talloc).on(st), edges.p, edges.p + ne, EdgeLess());
       CUDA_TRY(cudaMemcpyAsync(h.data(), edges.p, ne * sizeof(Edge), cudaMemcpyDeviceToHost, st));
       sync();
     }
@@ -1718,7 +1770,7 @@ struct nnm_dataset {
     stats.exact_evals += nc;
     double tau = INFINITY;
     if (nc >= P) {
-      thrust::sort(thrust::cuda::par.on(st), cands.p, cands.p + nc, CandLess());
+      thrust::sort(thrust::cuda::par(talloc).on(st), cands.p, cands.p + nc, CandLess());
       Cand c = read1(cands.p + (P - 1));
       tau = c.d;
     }
@@ -1730,7 +1782,7 @@ struct nnm_dataset {
     out.clear();
     if (na < 2) return;
     // deterministic order of the active set (atomics appended in arbitrary order)
-    thrust::sort(thrust::cuda::par.on(st), active.p, active.p + na);
+    thrust::sort(thrust::cuda::par(talloc).on(st), active.p, active.p + na);
     double lim = std::min(tau, thr);
     float bound = float_up(screen_upper(em, lim, 2.0 * maxnorm));
     DevBuf<float> bnd;
@@ -1747,7 +1799,7 @@ struct nnm_dataset {
     CUDA_TRY(cudaGetLastError());
     int64_t nk = (int64_t)read1(counters.p + 5);
     if (nk == 0) return;
-    thrust::sort(thrust::cuda::par.on(st), cands2.p, cands2.p + nk, CandLess());
+    thrust::sort(thrust::cuda::par(talloc).on(st), cands2.p, cands2.p + nk, CandLess());
     int64_t take = std::min<int64_t>(nk, P);
     out.resize(take);
     CUDA_TRY(cudaMemcpyAsync(out.data(), cands2.p, take * sizeof(Cand), cudaMemcpyDeviceToHost, st));
@@ -1796,6 +1848,11 @@ void init_device(int32_t device, int* sms) {
   if (prop.major < 10)
     throw NnmError{NNM_E_CUDA, std::string("libnnm is built for sm_100a; device is ") + prop.name};
   *sms = prop.multiProcessorCount;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
 }
 
 nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d, int32_t device) {
@@ -1818,6 +1875,8 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
     ds->ld = (n + TILE - 1) / TILE * TILE;
     ds->T = (int)(ds->ld / TILE);
     CUDA_TRY(cudaStreamCreateWithFlags(&ds->st, cudaStreamNonBlocking));
+    ds->stream_holder.st = ds->st;
+    t_alloc_stream = ds->st;
     CUDA_TRY(cudaEventCreate(&ds->ev0));
     CUDA_TRY(cudaEventCreate(&ds->ev1));
     if ((size_t)ds->d * TILE * 2 * sizeof(float) + 8192 > 200 * 1024)
@@ -1876,7 +1935,11 @@ int nnm_dataset_create_device(const double* X_dev, int64_t n, int32_t d, int32_t
 }
 
 int nnm_dataset_destroy(nnm_dataset* ds) {
-  return guarded([&] { delete ds; });
+  return guarded([&] {
+    if (!ds) return;
+    cudaSetDevice(ds->device);
+    delete ds;
+  });
 }
 
 int nnm_pairwise(int32_t metric, const double* x, int64_t nx, const double* y, int64_t ny,
@@ -1913,6 +1976,7 @@ int nnm_top_p(nnm_dataset* ds, int32_t metric, const int64_t* roots, const int64
     check_metric(metric);
     std::lock_guard<std::mutex> lk(ds->mu);
     CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
     const int64_t n = ds->n;
     std::vector<int> hc(ds->ld, -1), hs(ds->ld, 0);
     for (int64_t i = 0; i < n; ++i) {
@@ -1946,6 +2010,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
     if (P < 1) invalid("pairs_per_batch must be at least 1, got " + std::to_string(P));
     std::lock_guard<std::mutex> lk(ds->mu);
     CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
     auto t0 = std::chrono::steady_clock::now();
     const int64_t launches0 = g_launches.load();
     ds->stats = nnm_stats{};
@@ -1957,7 +2022,10 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
     if (!rounds_path) {
       // ---------------- Boruvka: exact MST of the eligible graph, then replay
       ds->stats.path = NNM_PATH_BORUVKA;
+      auto tp0 = std::chrono::steady_clock::now();
       ds->bv_begin(metric, cons->dmax);
+      ds->sync();
+      ds->stats.prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
       bool need = n > 1 && !(cons->kl1 > 0 && n <= cons->kl1);
       const char* pe = getenv("NNM_PRUNE");
       const bool prune = !(pe && pe[0] == '0');
@@ -1972,7 +2040,9 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
         int64_t added = ds->bv_finish_round(ds->B1.p, ds->B2.p);
         if (added == 0) break;
       }
+      auto tr0 = std::chrono::steady_clock::now();
       ds->bv_end(cons->kl1, out_merges, out_n_merges, out_assign, out_rounds, out_stop);
+      ds->stats.replay_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
     } else {
       // ---------------- top-P rounds with exact engine semantics
       ds->stats.path = NNM_PATH_ROUNDS;
@@ -2109,6 +2179,7 @@ int nnm_bv_begin(nnm_dataset* ds, int32_t metric, double dmax, int64_t* out_tile
     check_metric(metric);
     std::lock_guard<std::mutex> lk(ds->mu);
     CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
     ds->stats = nnm_stats{};
     ds->stats.path = NNM_PATH_BORUVKA;
     ds->bv_begin(metric, dmax);
@@ -2123,6 +2194,7 @@ int nnm_bv_scan(nnm_dataset* ds, int64_t w_begin, int64_t w_end, uint64_t* B1_de
     if (w_begin < 0 || w_end < w_begin || w_end > ds->tile_pairs()) invalid("bad tile-pair range");
     std::lock_guard<std::mutex> lk(ds->mu);
     CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
     CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
     ds->scan(ds->bv_metric, reinterpret_cast<unsigned long long*>(B1_dev),
              reinterpret_cast<unsigned long long*>(B2_dev), true, INT_UNSET, INT_UNSET,
@@ -2149,6 +2221,7 @@ int nnm_bv_second(nnm_dataset* ds, const uint64_t* B1loc, const uint64_t* B2loc,
     if (!ds) invalid("null dataset");
     std::lock_guard<std::mutex> lk(ds->mu);
     CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
     CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
     second_kernel<<<blocks_for(ds->n), 256, 0, ds->st>>>(
         (int)ds->n, reinterpret_cast<const unsigned long long*>(B1loc),
@@ -2166,6 +2239,7 @@ int nnm_bv_finish_round(nnm_dataset* ds, const uint64_t* B1_dev, const uint64_t*
     if (!ds) invalid("null dataset");
     std::lock_guard<std::mutex> lk(ds->mu);
     CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
     CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
     *out_edges = ds->bv_finish_round(reinterpret_cast<const unsigned long long*>(B1_dev),
                                      reinterpret_cast<const unsigned long long*>(B2_dev));
@@ -2179,6 +2253,7 @@ int nnm_bv_end(nnm_dataset* ds, int64_t kl1, nnm_merge* out_merges, int64_t* out
     if (kl1 == 0) invalid("kl1 must be a positive count, got 0");
     std::lock_guard<std::mutex> lk(ds->mu);
     CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
     ds->bv_end(kl1, out_merges, out_n_merges, out_assign, out_rounds, out_stop);
     if (stats) *stats = ds->stats;
   });
