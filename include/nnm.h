@@ -89,6 +89,8 @@ typedef struct {
   double prep_ms;          /* one-time per dataset/metric work done by this call (spatial view,
                               norms, tile balls); 0 when cached */
   double replay_ms;        /* edge sort + union-find replay into the merge log */
+  int64_t tc_items;        /* ordered 128x128 tile pairs run through the tensor-core scan
+                              (each a 128x128x32 kind::tf32 MMA); 0 on the FP32 path */
 } nnm_stats;
 
 int nnm_abi_version(void);
@@ -140,6 +142,12 @@ int nnm_bv_begin(nnm_dataset *ds, int32_t metric, double dmax, int64_t *out_tile
                  int64_t *out_rows);
 int nnm_bv_scan(nnm_dataset *ds, int64_t w_begin, int64_t w_end, uint64_t *B1_dev,
                 uint64_t *B2_dev);
+/* Pruned round scan: every rank evaluates the small phase-1 item
+ * list in full (so all ranks derive identical component bounds with no exchange)
+ * and its contiguous 1/world share of the phase-2 items; keys land in (B1, B2).
+ * world == 1 is the whole single-GPU pruned scan. */
+int nnm_bv_scan_pruned(nnm_dataset *ds, int32_t rank, int32_t world, uint64_t *B1_dev,
+                       uint64_t *B2_dev);
 /* B2 contribution for the global second-best: B2c[i] = (B1loc[i] == B1glob[i]) ? B2loc[i] : B1loc[i] */
 int nnm_bv_second(nnm_dataset *ds, const uint64_t *B1loc_dev, const uint64_t *B2loc_dev,
                   const uint64_t *B1glob_dev, uint64_t *B2c_dev);
@@ -154,6 +162,14 @@ int nnm_bv_end(nnm_dataset *ds, int64_t kl1, nnm_merge *out_merges, int64_t *out
  * Sustained FP32 (FFMA2) throughput of `device` in TFLOP/s: the roofline
  * denominator for the screening scan, which runs on the FP32 pipe. */
 int nnm_measure_fp32_peak(int32_t device, double *tflops);
+
+/* Error-model probe of the tensor-core screen (Euclidean, d <= 29): runs the scan
+ * kernel on the given tile pairs of the library's kd view (items: n_items (I, J)
+ * int32 pairs, tile indices < T where T(T+1)/2 is nnm_bv_begin's tile-pair count),
+ * dumps the accumulators and compares each real pair with its exact FP64 value.
+ * out[0] = max |v - S| / bound, out[1] = pairs whose key exceeds S (must be 0),
+ * out[2] = pairs checked.  Resets any staged Boruvka state of the dataset. */
+int nnm_tc_probe(nnm_dataset *ds, const int32_t *items, int64_t n_items, double *out);
 
 #ifdef __cplusplus
 }

@@ -34,8 +34,8 @@ STOP_NAMES = {1: "kl1-reached", 2: "no-eligible-pairs", 3: "single-cluster"}
 EXPORTED = (
     "nnm_abi_version", "nnm_last_error", "nnm_device_count", "nnm_dataset_create",
     "nnm_dataset_create_device", "nnm_dataset_destroy", "nnm_top_p", "nnm_run",
-    "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_second", "nnm_bv_finish_round",
-    "nnm_bv_end", "nnm_measure_fp32_peak",
+    "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_scan_pruned", "nnm_bv_second", "nnm_bv_finish_round",
+    "nnm_bv_end", "nnm_measure_fp32_peak", "nnm_tc_probe",
 )
 
 
@@ -50,7 +50,8 @@ class Stats(ctypes.Structure):
                 ("total_ms", ctypes.c_double), ("ambiguous_rows", ctypes.c_int64),
                 ("exact_evals", ctypes.c_int64), ("boruvka_rounds", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("pairs_covered", ctypes.c_double),
-                ("prep_ms", ctypes.c_double), ("replay_ms", ctypes.c_double)]
+                ("prep_ms", ctypes.c_double), ("replay_ms", ctypes.c_double),
+                ("tc_items", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -104,6 +105,8 @@ def load():
         lib.nnm_pairwise.argtypes = [i32, vp, i64, vp, i64, i32, i32, vp]
         lib.nnm_bv_begin.argtypes = [vp, i32, dbl, P(i64), P(i64)]
         lib.nnm_bv_scan.argtypes = [vp, i64, i64, vp, vp]
+        lib.nnm_bv_scan_pruned.argtypes = [vp, i32, i32, vp, vp]
+        lib.nnm_tc_probe.argtypes = [vp, vp, i64, P(dbl)]
         lib.nnm_bv_second.argtypes = [vp, vp, vp, vp, vp]
         lib.nnm_bv_finish_round.argtypes = [vp, vp, vp, P(i64)]
         lib.nnm_bv_end.argtypes = [vp, i64, vp, P(i64), vp, P(i64), P(i32), P(Stats)]

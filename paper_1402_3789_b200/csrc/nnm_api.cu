@@ -33,6 +33,7 @@
 #include "../../include/nnm.h"
 #include "nnm_common.cuh"
 #include "nnm_kernels.cuh"
+#include "nnm_tc.cuh"
 
 using namespace nnm;
 
@@ -666,6 +667,14 @@ __global__ void enum_write_kernel(const unsigned char* __restrict__ keep,
   }
 }
 
+__global__ void count_diag_kernel(const int2* __restrict__ items, int64_t cnt,
+                                  unsigned long long* acc) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned v = (t < cnt && items[t].x == items[t].y) ? 1u : 0u;
+  v = __reduce_add_sync(0xFFFFFFFFu, v);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(acc, (unsigned long long)v);
+}
+
 __global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt,
                                   const int* __restrict__ tcount, unsigned long long* acc) {
   // real point pairs covered by a list of tile pairs (for the stats)
@@ -1099,6 +1108,11 @@ struct nnm_dataset {
   int64_t vn = 0, vld = 0;
   int vT = 0;
   const int* cur_tcount = nullptr;
+  // tensor-core scan (Euclidean Boruvka, d <= TC_MAX_D; nnm_tc.cu)
+  bool tc_on = false;
+  bool tc_ready = false;
+  DevBuf<float> tc_img, tc_tnorm, tc_eta, tc_meta;
+  DevBuf<int2> tc_items;
   // dot form
   bool dot_on = false;
   DotModel dm{};
@@ -1211,6 +1225,11 @@ struct nnm_dataset {
       fill_none(b1, vn);
       if (b2) fill_none(b2, vn);
     }
+    if (tc_on && items && b2 && top2 && cur_X32 == X32p.p && kl2 == INT_UNSET &&
+        kl3 == INT_UNSET) {
+      tc_scan(b1, b2, thr_hi, w_begin, w_end, items);
+      return;
+    }
     tile_range.ensure(vT);
     tile_range_kernel<<<vT, TILE, 0, st>>>(comp.p, vn, vT, tile_range.p); note_launch();
     const int ksum = size_rule(kl2, kl3);
@@ -1262,6 +1281,98 @@ struct nnm_dataset {
     } else {  // unordered real pairs covered by this range of the triangle
       stats.pairs_evaluated += (double)n * (double)(n - 1) / 2.0 * ((double)(w_end - w_begin) / (double)tile_pairs());
     }
+  }
+
+  // operand image + bounds of the kd view for the tensor-core scan (once per dataset)
+  void tc_prepare() {
+    if (tc_ready) return;
+    tc_img.ensure((size_t)Tp * TC_TILE_FLOATS);
+    tc_tnorm.ensure(np_);
+    tc_eta.ensure(np_);
+    tc_meta.ensure((size_t)Tp * TC_META);
+    CUDA_TRY(launch_tc_prepare(X64p.p, porig.p, tcenter.p, normp.p, np_, d, Tp, tc_img.p,
+                               tc_tnorm.p, tc_eta.p, tc_meta.p, st));
+    note_launch();
+    note_launch();
+    tc_ready = true;
+  }
+
+  // tensor-core screening scan of the listed (upper-triangular) tile pairs: the list
+  // is mirrored to the full square and sorted by row tile, then scanned row-wise
+  void tc_scan(unsigned long long* b1, unsigned long long* b2, float thr_hi, int64_t w_begin,
+               int64_t w_end, const int2* items) {
+    const int64_t n_up = w_end - w_begin;
+    if (n_up <= 0) return;
+    tc_prepare();
+    tc_items.ensure((size_t)2 * n_up);
+    CUDA_TRY(launch_tc_mirror(items + w_begin, n_up, tc_items.p, st));
+    note_launch();
+    auto* k64 = reinterpret_cast<unsigned long long*>(tc_items.p);
+    thrust::sort(thrust::cuda::par(talloc).on(st), k64, k64 + 2 * n_up, ItemLess());
+    // diagonal items left a sentinel each (sorted last): count the real ones
+    counters.ensure(8);
+    CUDA_TRY(cudaMemsetAsync(counters.p + 5, 0, sizeof(unsigned long long), st));
+    count_diag_kernel<<<blocks_for(n_up), 256, 0, st>>>(items + w_begin, n_up, counters.p + 5); note_launch();
+    const int64_t nfull = 2 * n_up - (int64_t)read1(counters.p + 5);
+    TcArgs a;
+    a.img = tc_img.p;
+    a.tnorm = tc_tnorm.p;
+    a.eta = tc_eta.p;
+    a.meta = tc_meta.p;
+    a.comp = comp.p;
+    a.X64 = X64p.p;
+    a.np = (int)np_;
+    a.d = d;
+    a.T = Tp;
+    a.items = tc_items.p;
+    a.w_begin = 0;
+    a.w_end = nfull;
+    a.thr_hi = thr_hi;
+    a.B1 = b1;
+    a.B2 = b2;
+    a.dump = nullptr;
+    const char* dbg = getenv("NNM_TC_DBG");
+    a.dbg = dbg ? atoi(dbg) : 0;
+    const int grid = (int)std::min<int64_t>(nfull, (int64_t)sms);
+    const char* trf = getenv("NNM_TC_TRACE");
+    DevBuf<long long> trbuf;
+    a.trace = nullptr;
+    if (trf && nfull / grid >= 256) {
+      trbuf.ensure(8 * 256 * 2);
+      CUDA_TRY(cudaMemsetAsync(trbuf.p, 0, 8 * 256 * 2 * sizeof(long long), st));
+      a.trace = trbuf.p;
+    }
+    CUDA_TRY(cudaEventRecord(ev0, st));
+    CUDA_TRY(launch_tc_scan(a, grid, st));
+    note_launch();
+    CUDA_TRY(cudaEventRecord(ev1, st));
+    CUDA_TRY(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+    stats.scan_ms += ms;
+    stats.scans += 1;
+    stats.tc_items += nfull;
+    if (a.trace) {  // append the timeline of this launch (CTA 0, first 256 items)
+      std::vector<long long> h(8 * 256 * 2);
+      CUDA_TRY(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      sync();
+      if (FILE* f = fopen(trf, "a")) {
+        fprintf(f, "launch items %lld grid %d\n", (long long)nfull, grid);
+        const long long t0 = h[0];
+        for (int q = 0; q < 256; ++q)
+          fprintf(f, "%d prod %lld mma %lld prep %lld %lld epi_prepped %lld epi %lld %lld | ld %lld sums %lld tail %lld dn %lld fence %lld\n", q,
+                  h[(0 * 256 + q) * 2] - t0, h[(1 * 256 + q) * 2] - t0, h[(2 * 256 + q) * 2] - t0,
+                  h[(2 * 256 + q) * 2 + 1] - t0, h[(4 * 256 + q) * 2] - t0,
+                  h[(3 * 256 + q) * 2] - t0, h[(3 * 256 + q) * 2 + 1] - t0,
+                  h[(5 * 256 + q) * 2] - t0, h[(5 * 256 + q) * 2 + 1] - t0, h[(6 * 256 + q) * 2] - t0,
+                  h[(6 * 256 + q) * 2 + 1] - t0, h[(7 * 256 + q) * 2] - t0);
+        fclose(f);
+      }
+    }
+    counters.ensure(8);
+    CUDA_TRY(cudaMemsetAsync(counters.p + 7, 0, sizeof(unsigned long long), st));
+    item_pairs_kernel<<<blocks_for(n_up), 256, 0, st>>>(items + w_begin, n_up, cur_tcount, counters.p + 7); note_launch();
+    stats.pairs_evaluated += (double)read1(counters.p + 7);
   }
 
   // collect pairs (row list x columns) with screened value <= per-row bound
@@ -1351,10 +1462,14 @@ struct nnm_dataset {
     const char* de = getenv("NNM_DOT");
     dot_on = (metric == EUCLIDEAN || metric == SQEUCLIDEAN) && !(de && de[0] == '0') &&
              scan_use_ws(d);
+    const char* te = getenv("NNM_TC");
+    tc_on = (metric == EUCLIDEAN || metric == SQEUCLIDEAN) && tc_supported(d) &&
+            !(te && te[0] == '0');
     if (!std::isnan(dmax)) {
       bv_thr = metric == EUCLIDEAN ? dmax * dmax : dmax;  // metrics.py:93-103
       // dot-form keys are lower bounds of S: compare them with thr itself
-      bv_thr_hi = dot_on ? float_up(bv_thr) : float_up(screen_upper(em, bv_thr, 2.0 * maxnorm));
+      bv_thr_hi = (dot_on || tc_on) ? float_up(bv_thr)
+                                    : float_up(screen_upper(em, bv_thr, 2.0 * maxnorm));
     }
     comp.ensure(vn);
     fill_comp_view_kernel<<<blocks_for(vn), 256, 0, st>>>(porig.p, vn, comp.p); note_launch();
@@ -1551,7 +1666,14 @@ struct nnm_dataset {
 
   // One pruned Boruvka scan: exact per-row keys for every row that can hold its
   // component's minimum edge.
-  void pruned_scan(int metric) {
+  void pruned_scan(int metric) { pruned_scan_shard(metric, B1.p, B2.p, 0, 1); }
+
+  // Pruned scan into (b1, b2) where this rank evaluates the phase-1 items in full
+  // (small, replicated so every rank derives the same component bounds without an
+  // exchange) and its contiguous share [lo, hi) of the phase-2 items.  With world
+  // == 1 this is the whole pruned scan.  Phase-1 pairs are counted on rank 0 only.
+  void pruned_scan_shard(int metric, unsigned long long* b1, unsigned long long* b2, int rank,
+                         int world) {
     ensure_geometry(metric);
     tile_range.ensure(Tp);
     tile_range_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, Tp, tile_range.p); note_launch();
@@ -1561,18 +1683,21 @@ struct nnm_dataset {
       case CHEBYSHEV: pruned_lists<CHEBYSHEV>(n1, n2); break;
       default: pruned_lists<EUCLIDEAN>(n1, n2);
     }
-    fill_none(B1.p, vn);
-    fill_none(B2.p, vn);
-    if (n1 > 0) scan(metric, B1.p, B2.p, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
+    fill_none(b1, vn);
+    fill_none(b2, vn);
+    const double pe0 = stats.pairs_evaluated;
+    if (n1 > 0) scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
+    if (rank != 0) stats.pairs_evaluated = pe0;  // replicated phase 1 counts once per job
     ucomp.ensure(vn);
     fill_none(ucomp.p, vn);
     switch (metric) {
-      case MANHATTAN: ucomp_t<MANHATTAN>(B1.p); pruned_phase2<MANHATTAN>(n2); break;
-      case CHEBYSHEV: ucomp_t<CHEBYSHEV>(B1.p); pruned_phase2<CHEBYSHEV>(n2); break;
-      default: ucomp_t<EUCLIDEAN>(B1.p); pruned_phase2<EUCLIDEAN>(n2);
+      case MANHATTAN: ucomp_t<MANHATTAN>(b1); pruned_phase2<MANHATTAN>(n2); break;
+      case CHEBYSHEV: ucomp_t<CHEBYSHEV>(b1); pruned_phase2<CHEBYSHEV>(n2); break;
+      default: ucomp_t<EUCLIDEAN>(b1); pruned_phase2<EUCLIDEAN>(n2);
     }
-    if (n2 > 0) scan(metric, B1.p, B2.p, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n2, items2.p, false);
-    pairs_covered += (double)n * (double)(n - 1) / 2.0;
+    const int64_t lo2 = n2 * rank / world, hi2 = n2 * (rank + 1) / world;
+    if (hi2 > lo2) scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, lo2, hi2, items2.p, false);
+    if (rank == 0) pairs_covered += (double)n * (double)(n - 1) / 2.0;
     if (getenv("NNM_DEBUG")) {
       const int T = Tp;
       std::vector<double> rad(T), um(T);
@@ -1619,7 +1744,7 @@ struct nnm_dataset {
   void refine_t(const unsigned long long* b1, const unsigned long long* b2) {
     refine_kernel<M><<<blocks_for(vn), 256, 0, st>>>(X64p.p, (int)vn, d, b1, b2, normp.p, maxnormp, em,
                                                     bv_thr, rb_d.p, rb_j.p, rowlow.p, amb.p,
-                                                    counters.p + 1, porig.p, dot_on ? 1 : 0); note_launch();
+                                                    counters.p + 1, porig.p, (dot_on || tc_on) ? 1 : 0); note_launch();
   }
 
   int64_t bv_finish_round(const unsigned long long* b1, const unsigned long long* b2) {
@@ -2182,6 +2307,8 @@ int nnm_bv_begin(nnm_dataset* ds, int32_t metric, double dmax, int64_t* out_tile
     t_alloc_stream = ds->st;
     ds->stats = nnm_stats{};
     ds->stats.path = NNM_PATH_BORUVKA;
+    ds->stats.device = ds->device;
+    ds->pairs_covered = 0.0;
     ds->bv_begin(metric, dmax);
     if (out_tile_pairs) *out_tile_pairs = ds->tile_pairs();
     if (out_rows) *out_rows = ds->vn;
@@ -2215,6 +2342,74 @@ __global__ void second_kernel(int n, const unsigned long long* b1l, const unsign
 }  // namespace nnm
 
 extern "C" {
+int nnm_bv_scan_pruned(nnm_dataset* ds, int32_t rank, int32_t world, uint64_t* B1_dev,
+                       uint64_t* B2_dev) {
+  return guarded([&] {
+    if (!ds || !B1_dev || !B2_dev) invalid("null argument");
+    if (world < 1 || rank < 0 || rank >= world) invalid("bad rank / world");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
+    CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
+    ds->pruned_scan_shard(ds->bv_metric, reinterpret_cast<unsigned long long*>(B1_dev),
+                          reinterpret_cast<unsigned long long*>(B2_dev), rank, world);
+    ds->sync();
+  });
+}
+
+int nnm_tc_probe(nnm_dataset* ds, const int32_t* items, int64_t n_items, double* out) {
+  return guarded([&] {
+    if (!ds || !items || !out) invalid("null argument");
+    if (n_items < 1) invalid("n_items must be at least 1");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    CUDA_TRY(cudaSetDevice(ds->device));
+    t_alloc_stream = ds->st;
+    if (!tc_supported(ds->d)) throw NnmError{NNM_E_UNSUPPORTED, "d outside the tensor-core scan"};
+    ds->bv_begin(EUCLIDEAN, NAN);  // kd view, tile geometry, singleton components
+    ds->tc_prepare();
+    for (int64_t t = 0; t < 2 * n_items; ++t)
+      if (items[t] < 0 || items[t] >= ds->Tp) invalid("tile index out of range");
+    DevBuf<int2> it;
+    it.ensure(n_items);
+    DevBuf<float> dump;
+    dump.ensure((size_t)n_items * TILE * TILE);
+    DevBuf<unsigned long long> acc;
+    acc.ensure(3);
+    CUDA_TRY(cudaMemcpyAsync(it.p, items, n_items * sizeof(int2), cudaMemcpyHostToDevice, ds->st));
+    CUDA_TRY(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), ds->st));
+    TcArgs a{};
+    a.img = ds->tc_img.p;
+    a.tnorm = ds->tc_tnorm.p;
+    a.eta = ds->tc_eta.p;
+    a.meta = ds->tc_meta.p;
+    a.comp = ds->comp.p;
+    a.X64 = ds->X64p.p;
+    a.np = (int)ds->np_;
+    a.d = ds->d;
+    a.T = ds->Tp;
+    a.items = it.p;
+    a.w_begin = 0;
+    a.w_end = n_items;
+    a.thr_hi = INFINITY;
+    a.B1 = ds->B1.p;
+    a.B2 = ds->B2.p;
+    a.dump = dump.p;
+    a.dbg = 0;
+    a.trace = nullptr;
+    CUDA_TRY(launch_tc_scan(a, (int)std::min<int64_t>(n_items, ds->sms), ds->st));
+    CUDA_TRY(launch_tc_probe(a, ds->X64p.p, it.p, n_items, acc.p, ds->st));
+    unsigned long long h[3];
+    CUDA_TRY(cudaMemcpyAsync(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost, ds->st));
+    ds->sync();
+    float worst;
+    uint32_t wb = (uint32_t)h[0];
+    memcpy(&worst, &wb, 4);
+    out[0] = worst;
+    out[1] = (double)h[1];
+    out[2] = (double)h[2];
+  });
+}
+
 int nnm_bv_second(nnm_dataset* ds, const uint64_t* B1loc, const uint64_t* B2loc,
                   const uint64_t* B1glob, uint64_t* B2c) {
   return guarded([&] {
@@ -2223,8 +2418,8 @@ int nnm_bv_second(nnm_dataset* ds, const uint64_t* B1loc, const uint64_t* B2loc,
     CUDA_TRY(cudaSetDevice(ds->device));
     t_alloc_stream = ds->st;
     CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
-    second_kernel<<<blocks_for(ds->n), 256, 0, ds->st>>>(
-        (int)ds->n, reinterpret_cast<const unsigned long long*>(B1loc),
+    second_kernel<<<blocks_for(ds->vn), 256, 0, ds->st>>>(
+        (int)ds->vn, reinterpret_cast<const unsigned long long*>(B1loc),
         reinterpret_cast<const unsigned long long*>(B2loc),
         reinterpret_cast<const unsigned long long*>(B1glob),
         reinterpret_cast<unsigned long long*>(B2c)); note_launch();
@@ -2255,6 +2450,7 @@ int nnm_bv_end(nnm_dataset* ds, int64_t kl1, nnm_merge* out_merges, int64_t* out
     CUDA_TRY(cudaSetDevice(ds->device));
     t_alloc_stream = ds->st;
     ds->bv_end(kl1, out_merges, out_n_merges, out_assign, out_rounds, out_stop);
+    ds->stats.pairs_covered = ds->pairs_covered;
     if (stats) *stats = ds->stats;
   });
 }

@@ -1,0 +1,844 @@
+// nnm_tc.cu -- tensor-core screening scan for Euclidean Boruvka rounds (sm_100a).
+//
+// Replaces, for the Euclidean metric, the reference's distance + nearest-pair
+// selection stack (metrics.internal_pairwise -> scipy cdist, metrics.py:67-73;
+// pairgen._mask_ineligible / _chunk_candidates, pairgen.py:190-244) inside a
+// Boruvka round with a tcgen05 GEMM whose accumulator IS the screened distance:
+//
+//   every tile T is centred on its own fp32 centre c_T; x_t = tf32(fl(x32 - c_T))
+//   for a row point x (tile I) and a column point y (tile J), D = c_J - c_I:
+//     |x - y|^2 ~= v = r_i - 2 G'_ij,   r_i = |x_t - D|^2              (CUDA cores, per row)
+//     G'_ij = x_t . y_t + s_hi + s_lo,   s_hi + s_lo = -(|y_t|^2 + 2 D.y_t)/2
+//   G' is one M=128 x N=128 x K=32 kind::tf32 MMA: K holds the d coordinates,
+//   the (1, 1) x (s_hi, s_lo) column term, and component slots (-2^50 x 1) that
+//   push same-component pairs out of range.  The tf32 products are exact
+//   (x_t, y_t are tf32 values); the only rounding inside the tensor core is the
+//   fp32 accumulation.
+//
+// Rigorous filter: with E (squared-domain evaluation error) and eta (distance-domain
+// rounding of inputs / centring / tf32 / D), L = (sqrt(v - E) - eta)^2 <= S, the
+// exact scipy value.  A pair is skipped only when L exceeds the row's current
+// second-best key; a pair that passes gets its exact FP64 value (rounded down) as
+// key.  Keys stay lower bounds of S (the FP32 dot form's contract, nnm_common.cuh
+// DotModel), so refine / certification / ambiguity handling is unchanged -- and
+// since inserted keys are exact, rows are ambiguous only at true FP64 near-ties.
+//
+// Selection: the full square of the pruned tile-pair list is scanned (each
+// unordered tile pair as (I, J) and (J, I)), so a thread owns one row of the
+// accumulator (TMEM lane) and keeps that row's top-2 in registers for the whole
+// row tile: a 128-column block costs 4 tcgen05.ld + 43 FMNMX3 + 1 compare per
+// row; only blocks whose maximum G' passes the row threshold take the exact
+// (FP64-bounded) insert path.
+//
+// Warp roles (320 threads, 1 CTA / SM, persistent over a contiguous item range):
+//   warps 0-3  epilogue (TMEM lane quadrant = warp): thresholds, filter, top-2
+//   warps 4-7  prep: row-tile slots, per-item D, s_j and column slots into smem
+//   warp 8     producer: 16 KB bulk copies (cp.async.bulk) of operand tiles
+//   warp 9     MMA issuer + TMEM owner (2 accumulators x 128 columns)
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "nnm_common.cuh"
+#include "nnm_tc.cuh"
+
+namespace nnm {
+namespace {
+
+constexpr int TC_STAGES = 8;
+constexpr int TC_EPI_WARPS = 8;                        // warps 0-7: 2 groups x 4 lane quadrants
+constexpr int TC_EPI_GROUPS = 2;                       // epilogue groups, alternating items
+constexpr int TC_PREP_GROUPS = 2;                      // 2 x 2 prep warps, alternating items
+constexpr int TC_PREP_THREADS = 64;                    // per group; each thread owns 2 columns
+constexpr int TC_PRODUCER_WARP = TC_EPI_WARPS + TC_PREP_GROUPS * TC_PREP_THREADS / 32;
+constexpr int TC_MMA_WARP = TC_PRODUCER_WARP + 1;
+constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;     // 448: <= 4 warps per SMSP -> 128 regs
+constexpr int TC_RING = 64;                            // item ring (>> stages: see prep)
+constexpr int TC_ACC = 4;                              // TMEM accumulators (4 x 128 columns)
+constexpr uint32_t TC_TILE_BYTES = TC_TILE_FLOATS * 4;
+constexpr float TC_MASK = -1125899906842624.0f;   // -2^50: component-slot weight (A side)
+constexpr float TC_PAD = -1152921504606846976.0f; // -2^60: s_hi of a pad column
+constexpr float TC_U = 5.9604644775390625e-08f;   // 2^-24
+// tensor-core fp32 accumulation error per unit of sum |terms|: 2^-16, about 64x the
+// classical (K + 8) 2^-22 bound -- validated on the GPU by tests/test_tc.py
+constexpr float TC_CACC = 1.52587890625e-05f;
+
+struct TcSmem {
+  float A[2][TC_TILE_FLOATS];          // row-tile operand (+ per-row-tile tail)
+  float B[TC_STAGES][TC_TILE_FLOATS];  // column-tile operands (+ per-item tail)
+  float metaA[2][TC_META];             // tile records (centre, radius, eta bound)
+  float metaB[TC_STAGES][TC_META];
+  int acomp[2][TILE];                  // component labels of the row / column tiles
+  int bcomp[TC_STAGES][TILE];
+  float rrow[TC_STAGES][TILE];         // r_i of each row for the item in the stage
+  float dn[TC_STAGES];                 // |D| of the item
+  int2 ring[TC_RING];                  // (I, J) of item q at q % TC_RING (written by the producer)
+  int slot[2][8];
+  int slotcnt[TC_PREP_GROUPS][4];  // first-occurrence counts per 32-row block
+  unsigned long long full[TC_STAGES], prepped[TC_STAGES], empty[TC_STAGES];
+  unsigned long long tfull[TC_ACC], tempty[TC_ACC], afull[2], aprepped[2], aempty[2];
+  uint32_t tmem_base;
+};
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity), "r"(0x989680u)  // suspend-time hint: a waiting warp sleeps, it does not poll
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_spin(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void group_bar(int g) {  // the 64 threads of prep group g
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");
+}
+
+// K-major, 128-byte swizzled operand: rows of 128 B, 8-row atoms 1024 B apart (SBO),
+// descriptor version 1 (sm_100), layout type 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t sw128_desc(const void* p) {
+  const uint64_t a = su32(p);
+  return ((a >> 4) & 0x3FFFull) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
+constexpr uint32_t TC_IDESC =
+    (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(unsigned long long* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+      : "memory");
+}
+
+#define TC_R8(i) "=r"(r[i]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), \
+                 "=r"(r[i + 4]), "=r"(r[i + 5]), "=r"(r[i + 6]), "=r"(r[i + 7])
+__device__ __forceinline__ void tmem_ld32x(uint32_t taddr, float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : TC_R8(0), TC_R8(8), TC_R8(16), TC_R8(24)
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : TC_R8(0), TC_R8(8), TC_R8(16), TC_R8(24)
+      : "r"(taddr));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : TC_R8(32), TC_R8(40), TC_R8(48), TC_R8(56)
+      : "r"(taddr + 32));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+#undef TC_R8
+// timing trace (NNM_TC_TRACE): CTA 0 stamps clock64 per role / item / event
+__device__ __forceinline__ void trace(const TcArgs& p, int role, int q, int ev) {
+  if (p.trace && blockIdx.x == 0 && q < 256) p.trace[(role * 256 + q) * 2 + ev] = clock64();
+}
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// float offset of chunk c (4 floats) of row r inside a swizzled tile image
+__device__ __forceinline__ int swz(int r, int c) { return r * TC_K + ((c ^ (r & 7)) << 2); }
+
+__device__ __forceinline__ void insert_top2_g(unsigned long long* G1, unsigned long long* G2,
+                                              unsigned long long k1, unsigned long long k2) {
+  if (!key_valid(k1)) return;
+  const unsigned long long old = atomicMin(G1, k1);
+  const unsigned long long disp = (k1 < old) ? old : k1;
+  const unsigned long long m = disp < k2 ? disp : k2;
+  if (key_valid(m)) atomicMin(G2, m);
+}
+
+// Rigorous lower bound of S from the computed v (see file header): the |v| term
+// of the evaluation error is added here, E holds the rest.
+__device__ __forceinline__ float lower_key(float v, float E, float eta) {
+  const double w = (double)v - (double)E * (1.0 + 1e-9) - 1.02 * 5.9604644775390625e-08 * fabs((double)v);
+  if (!(w > 0.0)) return 0.f;
+  const double sq = sqrt(w) * (1.0 - 1e-15) - (double)eta;
+  if (!(sq > 0.0)) return 0.f;
+  return float_down(sq * sq * (1.0 - 1e-15));
+}
+
+// Tail of one operand row: positions d .. d+1+kc of the K = 32 floats (the image has
+// zeros beyond), written as whole 16-byte chunks (coordinates sharing the first chunk
+// are re-written unchanged).  A side (row tile): (1, 1, -2^50 per matching slot);
+// B side (column tile): (s_hi, s_lo, 1 per matching slot).  hits: bit k = slot k matches.
+// With a compile-time d every index below folds to a constant (straight-line code).
+__device__ __forceinline__ void write_tail(float* tile, int r, int d, int kc, float t0, float t1,
+                                          uint32_t hits, float hit) {
+  const int c0 = d >> 2, c1 = (d + 1 + kc) >> 2;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (c < c0 || c > c1) continue;
+    float4* q = reinterpret_cast<float4*>(tile + swz(r, c));
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+    if (c == c0 && (d & 3)) {
+      const float4 v = *q;
+      e[0] = v.x; e[1] = v.y; e[2] = v.z; e[3] = v.w;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = 4 * c + u - d;
+      const float val = t == 0 ? t0 : t == 1 ? t1 : ((hits >> ((t - 2) & 31)) & 1u) ? hit : 0.f;
+      e[u] = t < 0 ? e[u] : val;
+    }
+    *q = make_float4(e[0], e[1], e[2], e[3]);
+  }
+}
+
+__device__ __forceinline__ uint32_t slot_hits(int comp, const int (&slot)[8]) {
+  uint32_t h = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) h |= (comp >= 0 && comp == slot[k]) ? (1u << k) : 0u;
+  return h;
+}
+
+// One pass over the coordinates of an item for one row / column position:
+//   D = c_J - c_I (fp32), s = |y_t|^2 + 2 D.y_t, r = |x_t - D|^2, |D|
+// (independent partial sums per lane of a 4-chunk: any summation order is inside the
+// error bound).  Shared by the prep warps and the probe so both round identically.
+__device__ __forceinline__ void tc_item_sums(const float* __restrict__ mj, const float* __restrict__ mi,
+                                             const float* __restrict__ yrow_tile, int yr,
+                                             const float (&x)[32], int d, float& s_out,
+                                             float& r_out, float& dn_out) {
+  float s4[4] = {0.f, 0.f, 0.f, 0.f}, r4[4] = {0.f, 0.f, 0.f, 0.f}, n4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (4 * c >= d) continue;
+    const float4 a = *reinterpret_cast<const float4*>(mj + 4 * c);
+    const float4 b = *reinterpret_cast<const float4*>(mi + 4 * c);
+    const float4 y = *reinterpret_cast<const float4*>(yrow_tile + swz(yr, c));
+    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    const float yv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (4 * c + u >= d) continue;
+      const float dl = av[u] - bv[u];
+      s4[u] = fmaf(yv[u], yv[u] + 2.f * dl, s4[u]);
+      const float e = x[4 * c + u] - dl;
+      r4[u] = fmaf(e, e, r4[u]);
+      n4[u] = fmaf(dl, dl, n4[u]);
+    }
+  }
+  s_out = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  r_out = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+  dn_out = sqrtf((n4[0] + n4[1]) + (n4[2] + n4[3])) * 1.000001f;
+}
+
+// Squared-domain evaluation bound E of a row's pairs with tile J (all terms but the |v|
+// one, which lower_key adds) and the distance-domain rounding bound eta (file header).
+// sb bounds |s_j| = ||y_t|^2 + 2 D.y_t| through the tile radius RJ.
+__device__ __forceinline__ void tc_bounds(float r, float dnorm, int d, float tn_i, float eta_i,
+                                          float RJ, float etaJ, float& Erow, float& eta_row) {
+  const float sb = RJ * (RJ + 2.f * dnorm);
+  Erow = ((d + 3) * TC_U * 1.02f * r + (d + 2) * TC_U * 1.01f * sb + 2.4e-7f * sb +
+          2.f * TC_CACC * (tn_i * RJ + 0.51f * sb)) * 1.01f + 1e-30f;
+  eta_row = (eta_i + etaJ + TC_U * 1.001f * dnorm) * 1.0001f;
+}
+
+__device__ __forceinline__ void load_row(const float* tile, int r, int d, float (&x)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (4 * c < d) {
+      const float4 v = *reinterpret_cast<const float4*>(tile + swz(r, c));
+      x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+    } else {
+      x[4 * c] = x[4 * c + 1] = x[4 * c + 2] = x[4 * c + 3] = 0.f;
+    }
+  }
+}
+
+__device__ __forceinline__ float max32(const float* v) {
+  float t[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) t[k] = fmaxf(v[2 * k], v[2 * k + 1]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t[k] = fmaxf(t[2 * k], t[2 * k + 1]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t[k] = fmaxf(t[2 * k], t[2 * k + 1]);
+  return fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3]));
+}
+
+// Mask slots of a row tile: the first kc distinct components in position order
+// (parallel first-occurrence test + warp ballots).  Called by one prep group: thread
+// pt (0..63) owns rows pt and pt + 64.
+__device__ __forceinline__ void select_slots(const int* comp, int* slot, int* cnt, int g, int pt,
+                                             int kc) {
+  const int ca = comp[pt], cb = comp[pt + 64];
+  bool fa = ca >= 0, fb = cb >= 0;
+#pragma unroll 8
+  for (int r = 0; r < TILE; ++r) {
+    const int c = comp[r];
+    fa &= !(r < pt && c == ca);
+    fb &= !(r < pt + 64 && c == cb);
+  }
+  const unsigned ma = __ballot_sync(0xFFFFFFFFu, fa), mb = __ballot_sync(0xFFFFFFFFu, fb);
+  const int w = pt >> 5, lane = pt & 31;  // 32-row blocks in position order: a0 a1 b0 b1
+  if (lane == 0) {
+    cnt[w] = __popc(ma);
+    cnt[2 + w] = __popc(mb);
+  }
+  group_bar(g);
+  const unsigned below = (1u << lane) - 1u;
+  const int ra = __popc(ma & below) + (w ? cnt[0] : 0);
+  const int rb = __popc(mb & below) + cnt[0] + cnt[1] + (w ? cnt[2] : 0);
+  const int total = cnt[0] + cnt[1] + cnt[2] + cnt[3];
+  if (fa && ra < kc) slot[ra] = ca;
+  if (fb && rb < kc) slot[rb] = cb;
+  if (pt < 8 && pt >= min(total, kc)) slot[pt] = -2;
+}
+
+template <int DC>
+__global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // pointer arithmetic on the shared array keeps the shared state space (no generic LD/ST)
+  TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t total = p.w_end - p.w_begin;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = p.w_begin + (int64_t)blockIdx.x * per;
+  const int64_t w1 = min(w0 + per, p.w_end);
+  if (w0 >= w1) return;
+  const int nq = (int)(w1 - w0);
+  const int d = DC ? DC : p.d;  // compile-time for the specialised instantiations
+  const int kc = min(8, TC_K - d - 2);
+
+  if (tid == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.prepped[s], 1);
+      mbar_init(&S.empty[s], 1 + TC_EPI_WARPS / TC_EPI_GROUPS);
+    }
+    for (int a = 0; a < TC_ACC; ++a) {
+      mbar_init(&S.tfull[a], 1);
+      mbar_init(&S.tempty[a], TC_EPI_WARPS / TC_EPI_GROUPS);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&S.afull[a], 1);
+      mbar_init(&S.aprepped[a], 1);
+      mbar_init(&S.aempty[a], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == TC_MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     su32(&S.tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == TC_PRODUCER_WARP) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int rt = -1, prevI = -1;
+      int2 nxt = __ldg(p.items + w0);
+      for (int q = 0; q < nq; ++q) {
+        const int2 it = nxt;
+        if (q + 1 < nq) nxt = __ldg(p.items + w0 + q + 1);  // one item of lookahead
+        if (it.x != prevI) {
+          ++rt;
+          prevI = it.x;
+          const int xb = rt & 1;
+          if (rt >= 2) mbar_wait(&S.aempty[xb], ((rt - 2) >> 1) & 1);
+          mbar_expect_tx(&S.afull[xb], TC_TILE_BYTES + TC_META * 4 + TILE * 4);
+          bulk_g2s(S.A[xb], p.img + (int64_t)it.x * TC_TILE_FLOATS, TC_TILE_BYTES, &S.afull[xb]);
+          bulk_g2s(S.metaA[xb], p.meta + (int64_t)it.x * TC_META, TC_META * 4, &S.afull[xb]);
+          bulk_g2s(S.acomp[xb], p.comp + (int64_t)it.x * TILE, TILE * 4, &S.afull[xb]);
+        }
+        const int s = q % TC_STAGES;
+        if (q >= TC_STAGES) mbar_wait(&S.empty[s], ((q / TC_STAGES) - 1) & 1);
+        trace(p, 0, q, 0);
+        S.ring[q % TC_RING] = it;  // published to the other roles by the full barrier
+        mbar_expect_tx(&S.full[s], TC_TILE_BYTES + TC_META * 4 + TILE * 4);
+        bulk_g2s(S.B[s], p.img + (int64_t)it.y * TC_TILE_FLOATS, TC_TILE_BYTES, &S.full[s]);
+        bulk_g2s(S.metaB[s], p.meta + (int64_t)it.y * TC_META, TC_META * 4, &S.full[s]);
+        bulk_g2s(S.bcomp[s], p.comp + (int64_t)it.y * TILE, TILE * 4, &S.full[s]);
+      }
+    }
+  } else if (warp == TC_MMA_WARP) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int rt = -1, prevI = -1;
+      for (int q = 0; q < nq; ++q) {
+        const int s = q % TC_STAGES;
+        mbar_wait(&S.prepped[s], (q / TC_STAGES) & 1);
+        const int2 it = S.ring[q % TC_RING];
+        if (it.x != prevI) {
+          if (rt >= 0) mma_commit(&S.aempty[rt & 1]);  // previous A buffer free once its MMAs land
+          ++rt;
+          prevI = it.x;
+          mbar_wait(&S.aprepped[rt & 1], (rt >> 1) & 1);
+        }
+        const int a = q % TC_ACC;
+        if (q >= TC_ACC) mbar_wait(&S.tempty[a], ((q / TC_ACC) - 1) & 1);
+        trace(p, 1, q, 0);
+        tc_after();
+        const uint64_t ad = sw128_desc(S.A[rt & 1]), bd = sw128_desc(S.B[s]);
+        const int reps = (p.dbg & 32) ? 8 : 1;  // timing experiment: repeat the MMAs
+        for (int rep = 0; rep < reps; ++rep) {
+#pragma unroll
+          for (int kk = 0; kk < TC_K / 8; ++kk)  // K = 8 tf32 (32 B) per instruction
+            mma_tf32(tmem + a * TILE, ad + 2 * kk, bd + 2 * kk, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&S.empty[s]);
+        mma_commit(&S.tfull[a]);
+      }
+    }
+  } else if (warp >= TC_EPI_WARPS) {
+    // ------------------------------------------------------------ prep groups
+    // group g preps items q = g, g + 2, ...; thread pt owns columns / rows pt and pt + 64.
+    // Row-tile changes are read from the item ring (entries q-2 .. q are still live: the
+    // producer runs at most TC_STAGES items ahead of the slowest consumer, TC_RING >> that)
+    const int g = (warp - TC_EPI_WARPS) / (TC_PREP_THREADS / 32);
+    const int pt = tid - TC_EPI_WARPS * 32 - g * TC_PREP_THREADS;
+    int rt = -1, myI = -1;
+    float xa[32], xb2[32];
+    int slot[8];
+    for (int q = g; q < nq; q += TC_PREP_GROUPS) {
+      const int s = q % TC_STAGES;
+      mbar_wait(&S.full[s], (q / TC_STAGES) & 1);
+      if (pt == 0) trace(p, 2, q, 0);
+      // row-tile index of item q (counted over all items, both groups)
+      const int I = S.ring[q % TC_RING].x;
+      const int Im1 = q >= 1 ? S.ring[(q - 1) % TC_RING].x : -1;
+      if (rt < 0) {
+        rt = 0;
+        for (int k = 1; k <= q; ++k) rt += S.ring[k % TC_RING].x != S.ring[(k - 1) % TC_RING].x;
+      } else {
+        const int Im2 = S.ring[(q - 2) % TC_RING].x;
+        rt += (Im1 != Im2) + (I != Im1);
+      }
+      const int xb = rt & 1;
+      if (I != myI) {
+        myI = I;
+        if (I != Im1) {
+          // first item of the row tile: this group prepares the A operand
+          mbar_wait(&S.afull[xb], (rt >> 1) & 1);
+          select_slots(S.acomp[xb], S.slot[xb], S.slotcnt[g], g, pt, kc);
+          group_bar(g);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) slot[k] = S.slot[xb][k];
+          load_row(S.A[xb], pt, d, xa);
+          load_row(S.A[xb], pt + 64, d, xb2);
+          write_tail(S.A[xb], pt, d, kc, 1.f, 1.f, slot_hits(S.acomp[xb][pt], slot), TC_MASK);
+          write_tail(S.A[xb], pt + 64, d, kc, 1.f, 1.f, slot_hits(S.acomp[xb][pt + 64], slot),
+                     TC_MASK);
+          fence_proxy_async();
+          group_bar(g);
+          if (pt == 0) mbar_arrive(&S.aprepped[xb]);
+        } else {
+          // the other group prepared it: wait, then take the slots and the rows
+          mbar_wait(&S.aprepped[xb], (rt >> 1) & 1);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) slot[k] = S.slot[xb][k];
+          load_row(S.A[xb], pt, d, xa);
+          load_row(S.A[xb], pt + 64, d, xb2);
+        }
+      }
+      if (p.dbg & 2) {  // timing experiment: no prep work
+        group_bar(g);
+        if (pt == 0) mbar_arrive(&S.prepped[s]);
+        continue;
+      }
+      if (pt == 0) trace(p, 5, q, 0);
+      float sa, ra, dn, sb, rb, dn2;
+      tc_item_sums(S.metaB[s], S.metaA[xb], S.B[s], pt, xa, d, sa, ra, dn);
+      tc_item_sums(S.metaB[s], S.metaA[xb], S.B[s], pt + 64, xb2, d, sb, rb, dn2);
+      if (pt == 0) trace(p, 5, q, 1);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int col = pt + 64 * half;
+        const float sj = half ? sb : sa;
+        const int cj = S.bcomp[s][col];
+        float hi, lo;
+        if (cj >= 0) {
+          const float hh = -0.5f * sj;
+          hi = tf32_rna(hh);
+          lo = tf32_rna(hh - hi);
+        } else {
+          hi = TC_PAD;
+          lo = 0.f;
+        }
+        write_tail(S.B[s], col, d, kc, hi, lo, slot_hits(cj, slot), 1.f);
+      }
+      S.rrow[s][pt] = ra;
+      S.rrow[s][pt + 64] = rb;
+      if (pt == 0) S.dn[s] = dn;
+      if (!(p.dbg & 4)) fence_proxy_async();  // (dbg 4: timing experiment only)
+      if (pt == 0) trace(p, 7, q, 0);
+      group_bar(g);
+      if (pt == 0) {
+        trace(p, 2, q, 1);
+        mbar_arrive(&S.prepped[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue warps
+    // group e = warp / 4 takes items q = e, e + 2, ... (two items in flight); warp w owns
+    // TMEM lane quadrant w % 4 (rows 32(w%4) ..) and all 128 columns of its items.  Each
+    // group keeps its own per-row top-2 for the row tile and merges it atomically.
+    const int e = warp >> 2;
+    const int i = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    int prevI = -1;
+    unsigned long long k1 = NONE_KEY, k2 = NONE_KEY;
+    float tn_i = 0.f, eta_i = 0.f, gT = INFINITY;
+    int ci = -1;
+    int64_t g = 0;
+    for (int q = e; q < nq; q += TC_EPI_GROUPS) {
+      const int s = q % TC_STAGES;
+      if (tid == 0) trace(p, 6, q, 0);
+      mbar_wait(&S.prepped[s], (q / TC_STAGES) & 1);
+      if (tid == 0) trace(p, 4, q, 0);
+      const int2 it = S.ring[q % TC_RING];
+      const int I = it.x, J = it.y;
+      if (I != prevI) {
+        if (prevI >= 0 && ci >= 0 && !p.dump) insert_top2_g(p.B1 + g, p.B2 + g, k1, k2);
+        prevI = I;
+        g = (int64_t)I * TILE + i;
+        ci = __ldg(p.comp + g);
+        tn_i = __ldg(p.tnorm + g);
+        eta_i = __ldg(p.eta + g);
+        const unsigned long long gb = *((volatile const unsigned long long*)(p.B2 + g));
+        gT = key_valid(gb) ? key_value(gb) : INFINITY;
+        k1 = k2 = NONE_KEY;
+      }
+      const float r = S.rrow[s][i];
+      float Erow, eta_row;
+      tc_bounds(r, S.dn[s], d, tn_i, eta_i, S.metaB[s][32], S.metaB[s][33], Erow, eta_row);
+      // G' threshold equivalent to "L <= T may hold" (vthr: largest v with L <= T)
+      auto gamma_of = [&](float T) -> float {
+        if (!(T < INFINITY)) return -INFINITY;
+        const float st = sqrtf(T) * 1.000001f + eta_row;
+        const float vthr = (st * st + Erow) * 1.00001f;
+        return (r - vthr) * 0.5f - (fabsf(r) + vthr) * 1e-6f - 1e-30f;
+      };
+      float T = fminf(fminf(k2 == NONE_KEY ? INFINITY : key_value(k2), gT), p.thr_hi);
+      float gam = gamma_of(T);
+      const int a = q % TC_ACC;
+      mbar_wait(&S.tfull[a], (q / TC_ACC) & 1);
+      if (tid == 0) trace(p, 3, q, 0);
+      tc_after();
+      if (!(p.dbg & 1)) {
+        bool want = false;
+#pragma unroll 1
+        for (int hb = 0; hb < 2; ++hb) {
+          float v[64];
+          tmem_ld64(lane_base + a * TILE + hb * 64, v);
+          if (p.dump) {
+            float* o = p.dump + ((w0 + q - p.w_begin) * TILE + i) * TILE + hb * 64;
+#pragma unroll
+            for (int jj = 0; jj < 64; ++jj) o[jj] = v[jj];
+          } else {
+            want |= fmaxf(max32(v), max32(v + 32)) >= gam;
+          }
+        }
+        if (!p.dump && __any_sync(0xFFFFFFFFu, ci >= 0 && want)) {
+          // exact insert path (rare): re-read this row's values one by one (a rolled
+          // loop keeps the code small); a pair whose screened lower bound can beat the
+          // row's second best gets its exact scipy-order FP64 value (rounded down) as key,
+          // so certification in refine is as sharp as the FP64 order allows
+          // (tcgen05.ld is warp-collective: every lane loads, each lane filters its own row)
+#pragma unroll 1
+          for (int j = 0; j < TILE; ++j) {
+            __syncwarp();
+            const float vj = tmem_ld1(lane_base + a * TILE + j);
+            if (ci < 0 || !(vj >= gam)) continue;
+            const int cj = S.bcomp[s][j];
+            if (cj < 0 || cj == ci) continue;
+            if (!(lower_key(__fmaf_rn(-2.f, vj, r), Erow, eta_row) <= T)) continue;
+            const int64_t gj = (int64_t)J * TILE + j;
+            const float L = float_down(exact_dist<EUCLIDEAN>(p.X64 + g * d, p.X64 + gj * d, d));
+            if (!(L <= p.thr_hi)) continue;
+            const unsigned long long key = ((unsigned long long)__float_as_uint(L) << 32) | (unsigned)gj;
+            if (key < k2) {
+              if (key < k1) {
+                k2 = k1;
+                k1 = key;
+              } else {
+                k2 = key;
+              }
+              T = fminf(fminf(key_value(k2), gT), p.thr_hi);
+              gam = gamma_of(T);
+            }
+          }
+        }
+      }
+      tc_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (tid == 0) trace(p, 3, q, 1);
+        mbar_arrive(&S.tempty[a]);
+        mbar_arrive(&S.empty[s]);
+      }
+    }
+    if (prevI >= 0 && ci >= 0 && !p.dump) insert_top2_g(p.B1 + g, p.B2 + g, k1, k2);
+  }
+
+  tc_before();
+  __syncthreads();
+  tc_after();
+  if (warp == TC_MMA_WARP)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// ---------------------------------------------------------------- operand image
+__global__ void tc_prepare_kernel(const double* __restrict__ X64p, const int* __restrict__ porig,
+                                  const double* __restrict__ tcenter64,
+                                  const double* __restrict__ normp, int64_t np, int d,
+                                  float* __restrict__ img, float* __restrict__ tnorm,
+                                  float* __restrict__ eta, float* __restrict__ meta) {
+  const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= np) return;
+  const int64_t T0 = pos / TILE;
+  const int r = (int)(pos % TILE);
+  if (r < TC_META && r != 32 && r != 33)  // centre (zero padded); tR / tEta: tc_tile_max_kernel
+    meta[T0 * TC_META + r] = r < d ? __double2float_rn(tcenter64[T0 * d + r]) : 0.f;
+  float xt[TC_K];
+#pragma unroll
+  for (int k = 0; k < TC_K; ++k) xt[k] = 0.f;
+  if (porig[pos] >= 0) {
+    double xc2 = 0.0, tn2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < TC_K; ++k) {
+      if (k < d) {
+        const float x32 = __double2float_rn(X64p[pos * d + k]);
+        const float c = __double2float_rn(tcenter64[T0 * d + k]);
+        const float xc = __fsub_rn(x32, c);
+        const float t = tf32_rna(xc);
+        xt[k] = t;
+        xc2 += (double)xc * (double)xc;
+        tn2 += (double)t * (double)t;
+      }
+    }
+    const double u = 5.9604644775390625e-08;
+    tnorm[pos] = float_up(sqrt(tn2) * (1.0 + 1e-12));
+    eta[pos] = float_up((u * normp[pos] + (1.001 * u + 4.8828125e-04) * sqrt(xc2)) * 1.0001 + 1e-30);
+  } else {
+    tnorm[pos] = 0.f;
+    eta[pos] = 0.f;
+  }
+  float* o = img + T0 * TC_TILE_FLOATS;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<float4*>(o + swz(r, c)) =
+        make_float4(xt[4 * c], xt[4 * c + 1], xt[4 * c + 2], xt[4 * c + 3]);
+}
+
+__global__ void tc_tile_max_kernel(const float* __restrict__ tnorm, const float* __restrict__ eta,
+                                   float* __restrict__ meta) {
+  const int T0 = blockIdx.x;
+  float a = tnorm[(int64_t)T0 * TILE + threadIdx.x], b = eta[(int64_t)T0 * TILE + threadIdx.x];
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmaxf(a, __shfl_xor_sync(0xFFFFFFFFu, a, o));
+    b = fmaxf(b, __shfl_xor_sync(0xFFFFFFFFu, b, o));
+  }
+  __shared__ float sa[4], sb[4];
+  if ((threadIdx.x & 31) == 0) {
+    sa[threadIdx.x >> 5] = a;
+    sb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    meta[(int64_t)T0 * TC_META + 32] = fmaxf(fmaxf(sa[0], sa[1]), fmaxf(sa[2], sa[3]));
+    meta[(int64_t)T0 * TC_META + 33] = fmaxf(fmaxf(sb[0], sb[1]), fmaxf(sb[2], sb[3]));
+  }
+}
+
+__global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n, int2* __restrict__ out) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n) return;
+  const int2 it = items[w];
+  out[2 * w] = it;
+  out[2 * w + 1] = (it.x != it.y) ? make_int2(it.y, it.x) : make_int2(0x7FFFFFFF, 0x7FFFFFFF);
+}
+
+// Error-model probe: for dumped accumulators of `items`, compare the rigorous key L
+// and the bound with the exact scipy-order FP64 value S of every real, distinct pair.
+// out[0] = max |v - S| / bound (atomicMax on the bits of a nonnegative float),
+// out[1] = pairs with L > S (must be 0), out[2] = pairs checked.
+__global__ void tc_probe_kernel(TcArgs p, const double* __restrict__ X64p, const int2* __restrict__ items,
+                                int64_t nitems, unsigned long long* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nitems * TILE) return;
+  const int64_t q = t / TILE;
+  const int i = (int)(t % TILE);
+  const int2 it = items[q];
+  const int I = it.x, J = it.y, d = p.d;
+  const int64_t gi = (int64_t)I * TILE + i;
+  if (p.comp[gi] < 0) return;
+  float x[32];
+  load_row(p.img + (int64_t)I * TC_TILE_FLOATS, i, d, x);
+  float sj, r, dnorm;  // (sj unused: the column term is inside the dumped accumulator)
+  tc_item_sums(p.meta + (int64_t)J * TC_META, p.meta + (int64_t)I * TC_META,
+               p.img + (int64_t)J * TC_TILE_FLOATS, i, x, d, sj, r, dnorm);
+  float Erow, eta_row;
+  tc_bounds(r, dnorm, d, p.tnorm[gi], p.eta[gi], p.meta[(int64_t)J * TC_META + 32],
+            p.meta[(int64_t)J * TC_META + 33], Erow, eta_row);
+  float worst = 0.f;
+  unsigned long long bad = 0, cnt = 0;
+  for (int j = 0; j < TILE; ++j) {
+    const int64_t gj = (int64_t)J * TILE + j;
+    if (gj == gi || p.comp[gj] < 0 || p.comp[gj] == p.comp[gi]) continue;
+    const float G = p.dump[(q * TILE + i) * TILE + j];
+    const float v = __fmaf_rn(-2.f, G, r);
+    const float L = lower_key(v, Erow, eta_row);
+    double S = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double dd = __dsub_rn(X64p[gi * d + k], X64p[gj * d + k]);
+      S = __dadd_rn(S, __dmul_rn(dd, dd));
+    }
+    const double e = (double)eta_row;
+    const double bound = (double)Erow + 1.02 * 5.9604644775390625e-08 * fabs((double)v) +
+                         2.0 * e * sqrt(S) + e * e;
+    const float ratio = (float)(fabs((double)v - S) / bound);
+    worst = fmaxf(worst, ratio);
+    bad += ((double)L > S);
+    ++cnt;
+  }
+  atomicMax(out, (unsigned long long)__float_as_uint(worst));
+  if (bad) atomicAdd(out + 1, bad);
+  atomicAdd(out + 2, cnt);
+}
+
+}  // namespace
+
+cudaError_t launch_tc_probe(const TcArgs& a, const double* X64p, const int2* items, int64_t n,
+                            unsigned long long* out, cudaStream_t st) {
+  tc_probe_kernel<<<(unsigned)((n * TILE + 127) / 128), 128, 0, st>>>(a, X64p, items, n, out);
+  return cudaGetLastError();
+}
+
+size_t tc_smem_bytes() { return sizeof(TcSmem) + 1024; }
+
+bool tc_supported(int d) { return d >= 1 && d <= TC_MAX_D; }
+
+template <int DC>
+static cudaError_t launch_tc_d(const TcArgs& a, int grid, cudaStream_t st) {
+  const size_t sm = tc_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(tc_scan_kernel<DC>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[nnm] tc_scan smem attribute (%zu B) failed: %s\n", sm, cudaGetErrorString(e));
+    return e;
+  }
+  tc_scan_kernel<DC><<<grid, TC_THREADS, sm, st>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, tc_scan_kernel<DC>) == cudaSuccess)
+      fprintf(stderr, "[nnm] tc_scan launch failed: regs %d maxThreads %d smem %zu+%zu localBytes %zu\n",
+              fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, sm, fa.localSizeBytes);
+  }
+  return e;
+}
+
+cudaError_t launch_tc_scan(const TcArgs& a, int grid, cudaStream_t st) {
+  // the BASELINE shapes get compile-time d (straight-line tails); others run generic
+  if (a.d == 25) return launch_tc_d<25>(a, grid, st);
+  if (a.d == 8) return launch_tc_d<8>(a, grid, st);
+  return launch_tc_d<0>(a, grid, st);
+}
+
+cudaError_t launch_tc_prepare(const double* X64p, const int* porig, const double* tcenter64,
+                              const double* normp, int64_t np, int d, int T, float* img,
+                              float* tnorm, float* eta, float* meta, cudaStream_t st) {
+  tc_prepare_kernel<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(X64p, porig, tcenter64, normp, np,
+                                                                  d, img, tnorm, eta, meta);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  tc_tile_max_kernel<<<T, TILE, 0, st>>>(tnorm, eta, meta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_mirror(const int2* items, int64_t n, int2* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  tc_mirror_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(items, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace nnm

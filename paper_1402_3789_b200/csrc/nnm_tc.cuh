@@ -1,0 +1,52 @@
+// nnm_tc.cuh -- tensor-core (tcgen05, kind::tf32) screening scan for Euclidean
+// Boruvka rounds (internal interface; see nnm_tc.cu and DESIGN.md "TC scan").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "nnm_common.cuh"
+
+namespace nnm {
+
+constexpr int TC_K = 32;              // K extent of one operand row (floats): 128 B = one SW128 atom row
+constexpr int TC_TILE_FLOATS = TILE * TC_K;  // 4096 floats = 16 KB per tile image
+constexpr int TC_MAX_D = TC_K - 3;    // coords + (s_hi, s_lo) + >= 1 component slot
+constexpr int TC_META = 48;           // floats per tile record (192 B, bulk-copy aligned)
+
+struct TcArgs {
+  const float* img;       // [T][128][32] swizzled operand image: tf32-exact centred coords, 0 elsewhere
+  const float* tnorm;     // [np] |x_t| of each position, rounded up (0 for pads)
+  const float* eta;       // [np] distance-domain rounding bound of each position, rounded up
+  const float* meta;      // [T][TC_META] tile records: fp32 centre the image was centred on
+                          // (32, zero padded), max tnorm (32), max eta (33)
+  const int* comp;        // [np] component label per position (-1: pad)
+  const double* X64;      // [np][d] exact coordinates of the view (keys of inserted pairs)
+  int np, d, T;
+  const int2* items;      // ordered (row tile I, column tile J) pairs, sorted by I
+  int64_t w_begin, w_end;
+  float thr_hi;           // keys above this are ineligible (L units; +inf: no dmax)
+  unsigned long long* B1; // [np] best key per row (float_down(S) << 32 | partner position)
+  unsigned long long* B2; // [np] second-best key
+  float* dump;            // debug: raw accumulators [items][128][128] (nullptr in production)
+  long long* trace;       // NNM_TC_TRACE: [5 roles][256 items][2] clock64 stamps of CTA 0
+  int dbg;                // timing experiments (NNM_TC_DBG): 1 = no epilogue work, 2 = no prep work
+};
+
+size_t tc_smem_bytes();
+bool tc_supported(int d);
+cudaError_t launch_tc_scan(const TcArgs& a, int grid, cudaStream_t st);
+
+// Operand image + per-position / per-tile bounds for the kd view (once per dataset).
+cudaError_t launch_tc_prepare(const double* X64p, const int* porig, const double* tcenter64,
+                              const double* normp, int64_t np, int d, int T, float* img,
+                              float* tnorm, float* eta, float* meta, cudaStream_t st);
+
+// Error-model probe over dumped accumulators (a.dump filled by launch_tc_scan for `items`).
+cudaError_t launch_tc_probe(const TcArgs& a, const double* X64p, const int2* items, int64_t n,
+                            unsigned long long* out, cudaStream_t st);
+
+// Full-square item list: out[2w] = items[w], out[2w+1] = mirrored (J, I), or the sentinel
+// (INT_MAX, INT_MAX) for a diagonal item (it sorts last; the caller sorts by (I, J)).
+cudaError_t launch_tc_mirror(const int2* items, int64_t n, int2* out, cudaStream_t st);
+
+}  // namespace nnm

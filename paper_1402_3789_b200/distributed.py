@@ -1,11 +1,14 @@
 """Multi-GPU Boruvka driver: one process per GPU, torch.distributed for plumbing.
 
 Partitioning: every rank holds the whole dataset (X64 + FP32
-tiles, 600 MB at 2M x 25); the upper-triangular tile-pair space
-[0, T(T+1)/2) is split into contiguous equal-count ranges, one per rank.  Per
-Boruvka round each rank scans its range into per-row keys (B1 best, B2
-second best; u64 = fp32 bits << 32 | partner), then two all-reduce(MIN) calls
-combine them:
+tiles, 600 MB at 2M x 25).  Each Boruvka round is the pruned scan of DESIGN.md
+3.1: every rank evaluates the small phase-1 tile-pair list in full (so all
+ranks derive the same component bounds and the same phase-2 list without an
+exchange) and a contiguous equal-count 1/world share of the phase-2 tile pairs
+(``nnm_bv_scan_pruned``).  ``pruned=False`` splits the dense upper-triangular
+tile-pair space [0, T(T+1)/2) instead (``nnm_bv_scan``).  Each rank scans into
+per-row keys (B1 best, B2 second best; u64 = fp32 bits << 32 | partner), then
+two all-reduce(MIN) calls combine them:
 
     B1 = min_r B1_r
     B2 = min_r (B1_r == B1 ? B2_r : B1_r)      # second smallest of the union
@@ -43,7 +46,8 @@ def combine_second(b1_local, b2_local, b1_global):
     return torch.where(b1_local == b1_global, b2_local, b1_local)
 
 
-def run_boruvka_distributed(X, *, metric="euclidean", dmax=None, kl1=None, group=None):
+def run_boruvka_distributed(X, *, metric="euclidean", dmax=None, kl1=None, group=None,
+                            pruned=True):
     """Full-dendrogram NNM on all ranks of `group` (NCCL); every rank returns the same
     (merges, assignments, rounds, stop_reason, stats).  Inputs are replicated."""
     import torch
@@ -52,10 +56,12 @@ def run_boruvka_distributed(X, *, metric="euclidean", dmax=None, kl1=None, group
 
     dd = _native.DeviceDataset(np.ascontiguousarray(X, dtype=np.float64),
                                device=torch.cuda.current_device())
-    return run_boruvka_distributed_handle(dd, metric=metric, dmax=dmax, kl1=kl1, group=group)
+    return run_boruvka_distributed_handle(dd, metric=metric, dmax=dmax, kl1=kl1, group=group,
+                                          pruned=pruned)
 
 
-def run_boruvka_distributed_handle(dd, *, metric="euclidean", dmax=None, kl1=None, group=None):
+def run_boruvka_distributed_handle(dd, *, metric="euclidean", dmax=None, kl1=None, group=None,
+                                   pruned=True):
     """As run_boruvka_distributed, on an already resident DeviceDataset."""
     import time
 
@@ -82,7 +88,11 @@ def run_boruvka_distributed_handle(dd, *, metric="euclidean", dmax=None, kl1=Non
     added = ctypes.c_int64()
     need = n > 1 and not (kl1 is not None and n <= kl1)
     while need:
-        _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
+        if pruned:
+            _native.check(lib.nnm_bv_scan_pruned(dd.handle, rank, world, b1.data_ptr(),
+                                                 b2.data_ptr()))
+        else:
+            _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
         torch.cuda.synchronize()
         g1.copy_(b1)
         dist.all_reduce(g1, op=dist.ReduceOp.MIN, group=group)

@@ -144,8 +144,10 @@ def test_boruvka_vs_oracle_flat(nnm, metric, kind):
         assert np.array_equal(res.assignments, a_or), cons
 
 
-def test_staged_multi_range_equals_single(nnm):
-    """Emulate R ranks on one GPU: disjoint tile-pair ranges + min-combine of keys."""
+@pytest.mark.parametrize("pruned", [False, True])
+def test_staged_multi_range_equals_single(nnm, pruned):
+    """Emulate R ranks on one GPU: disjoint tile-pair shares (dense ranges, or the
+    pruned scan's phase-2 shares) + min-combine of keys."""
     import ctypes
 
     from paper_1402_3789_b200 import _native
@@ -167,7 +169,11 @@ def test_staged_multi_range_equals_single(nnm):
             lo, hi = shard_range(tp.value, r, R)
             b1 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
             b2 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
-            _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
+            if pruned:
+                _native.check(lib.nnm_bv_scan_pruned(dd.handle, r, R, b1.data_ptr(),
+                                                     b2.data_ptr()))
+            else:
+                _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
             parts.append((b1, b2))
         torch.cuda.synchronize()
         g1 = torch.stack([p[0] for p in parts]).min(0).values
