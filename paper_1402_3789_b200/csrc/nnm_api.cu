@@ -101,6 +101,27 @@ struct DevBuf {
   }
 };
 
+template <class T>
+struct PinnedBuf {  // grow-only page-locked host staging buffer
+  T* p = nullptr;
+  size_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  T* ensure(size_t count) {
+    if (count <= n && p) return p;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    CUDA_TRY(cudaMallocHost((void**)&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+    return p;
+  }
+};
+
 std::atomic<int64_t> g_launches{0};  // libnnm kernel launches (process-wide)
 inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
@@ -347,6 +368,25 @@ struct EdgeLess {
   }
 };
 
+struct ReplayEdge {  // host-side replay record (sorted order)
+  double dist;        // reported distance (sqrt for euclidean)
+  int a, b, round, pad;
+};
+
+__global__ void replay_edges_kernel(const Edge* __restrict__ e, int64_t ne, int sqrt_dist,
+                                    ReplayEdge* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ne) return;
+  const Edge x = e[t];
+  ReplayEdge r;
+  r.dist = sqrt_dist ? sqrt(x.d) : x.d;  // IEEE sqrt, as np.sqrt (metrics.py:86-90)
+  r.a = x.a;
+  r.b = x.b;
+  r.round = x.round;
+  r.pad = 0;
+  out[t] = r;
+}
+
 __global__ void hook_kernel(int n, const int* __restrict__ comp,
                             const unsigned long long* __restrict__ cmin_d,
                             const unsigned long long* __restrict__ cmin_ab, int* parent,
@@ -494,23 +534,72 @@ __device__ __forceinline__ bool same_single(const int2* __restrict__ tr, int I, 
   return a.x == a.y && b.x == b.y && a.x == b.x;
 }
 
+// FP32 SoA tile centres for the O(T^2) tile-level passes: c32[k][T], cn = metric norm of
+// c32 (rounded up), r32 = radius rounded up.
+template <int M>
+__global__ void centers32_kernel(const double* __restrict__ centers, const double* __restrict__ radius,
+                                 int T, int d, float* __restrict__ c32, float* __restrict__ cn,
+                                 float* __restrict__ r32) {
+  const int J = blockIdx.x * blockDim.x + threadIdx.x;
+  if (J >= T) return;
+  double nrm = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const float c = __double2float_rn(centers[(int64_t)J * d + k]);
+    c32[(int64_t)k * T + J] = c;
+    const double a = fabs((double)c);
+    if (M == EUCLIDEAN || M == SQEUCLIDEAN) nrm += a * a;
+    else if (M == MANHATTAN) nrm += a;
+    else nrm = fmax(nrm, a);
+  }
+  if (M == EUCLIDEAN || M == SQEUCLIDEAN) nrm = sqrt(nrm);
+  cn[J] = float_up(nrm * (1.0 + 1e-12));
+  r32[J] = float_up(radius[J]);
+}
+
+// metric distance of two fp32 centres (SoA), fp32 arithmetic
+template <int M>
+__device__ __forceinline__ float cdist32(const float* __restrict__ c32, int T, const float* ci, int J,
+                                         int d) {
+  float acc = 0.f;
+  for (int k = 0; k < d; ++k) {
+    const float t = fabsf(ci[k] - __ldg(c32 + (int64_t)k * T + J));
+    if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc = fmaf(t, t, acc);
+    else if (M == MANHATTAN) acc += t;
+    else acc = fmaxf(acc, t);
+  }
+  return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? sqrtf(acc) : acc;
+}
+
+// rigorous lower bound (internal units) of every pair of tile pair (I, J) from the fp32
+// centre distance: fp32 evaluation error <= (d+4)u dc, centre rounding <= u (|c_I|+|c_J|)
+template <int M>
+__device__ __forceinline__ double tile_lb32(float dc, float cnI, float cnJ, float rI, float rJ, int d) {
+  const double u = 5.9604644775390625e-08;
+  const double lo = (double)dc * (1.0 - (d + 4) * u) - 1.01 * u * ((double)cnI + (double)cnJ);
+  const double r = lo * (1.0 - 1e-9) - (double)rI - (double)rJ;
+  if (!(r > 0.0)) return 0.0;
+  return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? r * r * (1.0 - 1e-9) : r * (1.0 - 1e-9);
+}
+
 // Phase 1: for each tile I the PK tile pairs with the smallest LB among tiles
 // that can hold a cross-component pair with I (every pair of I x J in one
 // component is useless).  Seeds the component upper bounds.
 constexpr int PK = 8;
 template <int M>
-__global__ void phase1_kernel(const double* __restrict__ centers, const double* __restrict__ radius,
+__global__ void phase1_kernel(const float* __restrict__ c32, const float* __restrict__ r32,
                               const int2* __restrict__ trange, int T, int d, int2* __restrict__ out) {
   const int I = blockIdx.x;
+  __shared__ float ci[256];
+  for (int k = threadIdx.x; k < d; k += blockDim.x) ci[k] = c32[(int64_t)k * T + I];
+  __syncthreads();
   double bl[2] = {INFINITY, INFINITY};
   int bj[2] = {-1, -1};
   for (int J = threadIdx.x; J < T; J += blockDim.x) {
     if (same_single(trange, I, J)) continue;
     // rank by distance from I's centre to J's ball (the tile itself first): the
-    // LB alone ties at 0 for every overlapping ball
-    double lb = (J == I) ? -INFINITY
-                         : metric_dist_real<M>(centers + (int64_t)I * d, centers + (int64_t)J * d, d) -
-                               radius[J];
+    // LB alone ties at 0 for every overlapping ball.  A heuristic seed order (any
+    // choice is sound): fp32, deterministic (ties by J)
+    double lb = (J == I) ? -INFINITY : (double)(cdist32<M>(c32, T, ci, J, d) - r32[J]);
     if (lb < bl[1] || (lb == bl[1] && J < bj[1])) {
       if (lb < bl[0] || (lb == bl[0] && J < bj[0])) {
         bl[1] = bl[0]; bj[1] = bj[0]; bl[0] = lb; bj[0] = J;
@@ -614,18 +703,26 @@ __global__ void tile_umax_kernel(const int* __restrict__ comp, int64_t n,
 
 // Phase 2 enumeration, pass 1: keep flags + per-row-tile counts.
 template <int M>
-__global__ void enum_count_kernel(const double* __restrict__ centers, const double* __restrict__ radius,
+__global__ void enum_count_kernel(const float* __restrict__ c32, const float* __restrict__ cn,
+                                  const float* __restrict__ r32,
                                   const int2* __restrict__ trange, const double* __restrict__ umax,
                                   const unsigned* __restrict__ bits, int T, int d,
                                   unsigned char* __restrict__ keep, int* __restrict__ counts) {
   const int I = blockIdx.x;
+  __shared__ float ci[256];
+  for (int k = threadIdx.x; k < d; k += blockDim.x) ci[k] = c32[(int64_t)k * T + I];
+  __syncthreads();
   const double uI = umax[I];
+  const float cnI = cn[I], rI = r32[I];
   int c = 0;
   const int64_t w0 = tri_index(T, I, I);
   for (int J = I + threadIdx.x; J < T; J += blockDim.x) {
     const int64_t w = w0 + (J - I);
     bool k = !((bits[w >> 5] >> (w & 31)) & 1u) && !same_single(trange, I, J);
-    if (k) k = tile_lb<M>(centers, radius, d, I, J) <= fmax(uI, umax[J]);
+    // kept iff the rigorous lower bound of the tile pair can reach either component
+    // bound (a kept superset costs work, never exactness)
+    if (k && J != I) k = tile_lb32<M>(cdist32<M>(c32, T, ci, J, d), cnI, cn[J], rI, r32[J], d) <=
+                         fmax(uI, umax[J]);
     keep[w] = k;
     c += k;
   }
@@ -1089,6 +1186,8 @@ struct nnm_dataset {
   DevBuf<float> resc_bound, gathered;
   DevBuf<unsigned long long> cmin_d, cmin_ab, counters;
   DevBuf<Edge> edges;
+  DevBuf<ReplayEdge> replay;
+  PinnedBuf<ReplayEdge> host_replay;
   DevBuf<int2> pairs;
   DevBuf<double> pair_d;
   DevBuf<int> flag;
@@ -1120,6 +1219,7 @@ struct nnm_dataset {
   // pruning
   int geom_metric = -1;
   DevBuf<double> tcenter, tradius, tumax;
+  DevBuf<float> tc32, tcn32, tr32;  // fp32 SoA tile centres / norms / radii (tile passes)
   DevBuf<int2> items1, items2;
   DevBuf<unsigned> pbits;
   DevBuf<unsigned char> pkeep;
@@ -1600,6 +1700,16 @@ struct nnm_dataset {
     }
     note_launch();
     CUDA_TRY(cudaGetLastError());
+    tc32.ensure((size_t)Tp * d);
+    tcn32.ensure(Tp);
+    tr32.ensure(Tp);
+    switch (kind) {
+      case MANHATTAN: centers32_kernel<MANHATTAN><<<blocks_for(Tp), 256, 0, st>>>(tcenter.p, tradius.p, Tp, d, tc32.p, tcn32.p, tr32.p); break;
+      case CHEBYSHEV: centers32_kernel<CHEBYSHEV><<<blocks_for(Tp), 256, 0, st>>>(tcenter.p, tradius.p, Tp, d, tc32.p, tcn32.p, tr32.p); break;
+      default: centers32_kernel<EUCLIDEAN><<<blocks_for(Tp), 256, 0, st>>>(tcenter.p, tradius.p, Tp, d, tc32.p, tcn32.p, tr32.p);
+    }
+    note_launch();
+    CUDA_TRY(cudaGetLastError());
     if (kind == EUCLIDEAN) {
       dm = make_dot_model(d);
       tcenter32.ensure((size_t)Tp * d);
@@ -1619,7 +1729,7 @@ struct nnm_dataset {
     const int64_t W = tile_pairs();
     // phase-1 seeds: PK nearest cross-capable tiles per tile
     items1.ensure((size_t)Tp * PK);
-    phase1_kernel<M><<<Tp, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, Tp, d, items1.p); note_launch();
+    phase1_kernel<M><<<Tp, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     auto* k64 = reinterpret_cast<unsigned long long*>(items1.p);  // (I, J) -> J << 32 | I order
     // sort by (I, J): int2 memory is {x=I, y=J}; as u64 little-endian = J << 32 | I -> swap to key
@@ -1647,8 +1757,8 @@ struct nnm_dataset {
     pkeep.ensure(W);
     pcount.ensure(Tp);
     poffset.ensure(Tp + 1);
-    enum_count_kernel<M><<<Tp, 256, 0, st>>>(tcenter.p, tradius.p, tile_range.p, tumax.p, pbits.p, Tp, d,
-                                             pkeep.p, pcount.p); note_launch();
+    enum_count_kernel<M><<<Tp, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
+                                             Tp, d, pkeep.p, pcount.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), pcount.p, pcount.p + Tp, poffset.p, 0LL);
     long long last_off = read1(poffset.p + (Tp - 1));
@@ -1811,24 +1921,29 @@ struct nnm_dataset {
   void bv_end(int64_t kl1, nnm_merge* out, int64_t* n_merges, int64_t* assign, int64_t* rounds,
               int32_t* stop) {
     unsigned long long ne = read1(counters.p);
-    std::vector<Edge> h(ne);
+    // sorted edges, reported distances computed on the device, copied into pinned memory
+    ReplayEdge* h = nullptr;
     if (ne > 0) {
       thrust::sort(thrust::cuda::par(talloc).on(st), edges.p, edges.p + ne, EdgeLess());
-      CUDA_TRY(cudaMemcpyAsync(h.data(), edges.p, ne * sizeof(Edge), cudaMemcpyDeviceToHost, st));
+      replay.ensure(ne);
+      replay_edges_kernel<<<blocks_for((int64_t)ne), 256, 0, st>>>(edges.p, (int64_t)ne,
+                                                                   bv_metric == EUCLIDEAN ? 1 : 0,
+                                                                   replay.p); note_launch();
+      CUDA_TRY(cudaGetLastError());
+      h = host_replay.ensure(ne);
+      CUDA_TRY(cudaMemcpyAsync(h, replay.p, ne * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st));
       sync();
     }
-    // union-find replay (model.py:109-187): union keeps the smaller root
-    std::vector<int64_t> par(n), sz(n, 1);
-    for (int64_t i = 0; i < n; ++i) par[i] = i;
-    auto find = [&](int64_t x) {
-      int64_t r = x;
-      while (par[r] != r) r = par[r];
-      while (par[x] != r) {
-        int64_t nx = par[x];
-        par[x] = r;
-        x = nx;
+    // union-find replay (model.py:109-187): union keeps the smaller root (int32 forest,
+    // path halving; roots are always the minimum index of their cluster)
+    std::vector<int32_t> par(n), sz(n, 1);
+    for (int64_t i = 0; i < n; ++i) par[i] = (int32_t)i;
+    auto find = [&](int32_t x) {
+      while (par[x] != x) {
+        par[x] = par[par[x]];
+        x = par[x];
       }
-      return r;
+      return x;
     };
     int64_t count = n, nm = 0;
     auto stop_of = [&](int64_t c) -> int {
@@ -1837,13 +1952,12 @@ struct nnm_dataset {
       return 0;
     };
     int reason = stop_of(count);
-    int64_t max_round = 0;
     if (!reason) {
       for (unsigned long long t = 0; t < ne; ++t) {
-        const Edge& e = h[t];
-        int64_t ra = find(e.a), rb = find(e.b);
+        const ReplayEdge& e = h[t];
+        const int32_t ra = find(e.a), rb = find(e.b);
         if (ra == rb) throw NnmError{NNM_E_CUDA, "boruvka produced a cycle (internal error)"};
-        int64_t keep = std::min(ra, rb), drop = std::max(ra, rb);
+        const int32_t keep = std::min(ra, rb), drop = std::max(ra, rb);
         par[drop] = keep;
         sz[keep] += sz[drop];
         --count;
@@ -1851,17 +1965,16 @@ struct nnm_dataset {
         m.round = e.round;
         m.root_a = keep;
         m.root_b = drop;
-        m.dist = bv_metric == EUCLIDEAN ? std::sqrt(e.d) : e.d;  // metrics.py:86-90
+        m.dist = e.dist;  // reported units (metrics.py:86-90)
         m.new_size = sz[keep];
         m.point_a = e.a;
         m.point_b = e.b;
-        max_round = std::max<int64_t>(max_round, e.round);
         reason = stop_of(count);
         if (reason) break;
       }
       if (!reason) reason = NNM_STOP_NO_ELIGIBLE;
     }
-    for (int64_t i = 0; i < n; ++i) assign[i] = find(i);
+    for (int64_t i = 0; i < n; ++i) assign[i] = find((int32_t)i);
     *n_merges = nm;
     *rounds = (n > 1 && stop_of(n) == 0) ? bv_round : 0;
     *stop = reason;
