@@ -11,10 +11,12 @@ keys, hooking, sort + replay of the 1,999,999 merges).
               resident in HBM (a DeviceDataset built before the timed region).
 * ``e2e``     the same metric through the public API (``engine.run``) with host
               buffers: float64 X uploaded, merge log + labels read back, every step.
-* ``roofline`` dominant kernel = the fused screening scan; algorithmic flops per
-              launch = n(n-1)/2 pairs x 3d flops (sub, mul, add per coordinate),
-              average launch time from CUDA events on the library's stream, peak =
-              FFMA2 microbenchmark on this GPU (libnnm nnm_measure_fp32_peak).
+* ``roofline`` dominant kernel = the fused screening scan (tcgen05 TF32 tensor-core
+              scan for Euclidean d <= 29); algorithmic flops = evaluated pairs x 3d
+              (sub, mul, add per coordinate) over the CUDA-event time of the scan
+              launches on the library's stream; peak = dense TF32 (1/2 of the measured
+              bf16 figure); the FP32-roofline fraction the north star quotes (against
+              the FFMA2 microbenchmark, nnm_measure_fp32_peak) is reported beside it.
 * ``cpu_baseline`` the C oracle (a port of the reference's round scan) on the
               host cores, one top-P round on a bounded row sample.
 
@@ -170,16 +172,23 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def _load_traffic_per_pair():
-    """DRAM bytes per evaluated pair of the scan kernel, from the committed ncu
-    capture (profiles/scan_traffic.json, one full dense launch)."""
-    p = os.path.join(ROOT, "profiles", "scan_traffic.json")
+def _load_traffic(name: str):
+    """DRAM bytes per unit of the scan kernel from a committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", name)
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_pair")
+            return json.load(open(p))
         except (OSError, ValueError):
             return None
     return None
+
+
+def _measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except (OSError, ValueError):
+        return {}
 
 
 def run_gpu(args) -> None:
@@ -283,21 +292,49 @@ def run_gpu(args) -> None:
     peak = ctypes.c_double()
     _native.check(lib.nnm_measure_fp32_peak(local, ctypes.byref(peak)))
     avg_launch_ms = scan_ms / max(scans, 1)
-    # algorithmic flops (3d per evaluated pair: d sub, d mul, d add) over the CUDA-event
-    # time of all scan launches (launch sizes differ once tile pairs are pruned)
     pairs_eval = sum(s["pairs_evaluated"] for s in stats)
-    achieved = pairs_eval * 3 * d / (scan_ms / 1e3) / 1e12
-    bpp = _load_traffic_per_pair()
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                "frac": achieved / peak.value if peak.value else None,
-                "traffic": (bpp * pairs_eval / max(scans, 1)) if bpp is not None else None,
-                "traffic_note": "dram bytes per launch = ncu dram__bytes_read+write per pair "
-                                "(profiles/scan_traffic.json) x average pairs per launch",
-                "kernel": "scan_reg_kernel (fused FP32 dot-form distance + eligibility + per-row "
-                          "top-2 threshold filter)",
-                "peak_source": "measured FFMA2 microbenchmark on this GPU (MEASURED_PEAKS.json has no FP32 entry)",
-                "avg_launch_ms": avg_launch_ms, "launches": scans,
-                "scan_share_of_step": scan_ms / (ms_dev * args.steps)}
+    tc_items = sum(s.get("tc_items", 0) for s in stats)
+    # algorithmic work: 3d flops per evaluated unordered pair (d sub, d mul, d add)
+    # over the CUDA-event time of all scan launches on the library's stream
+    alg_tflops = pairs_eval * 3 * d / (scan_ms / 1e3) / 1e12
+    if tc_items > 0:
+        # tensor-core scan: ordered 128x128 tile pairs, each one 128x128x32 kind::tf32 MMA
+        mp = _measured_peaks()
+        bf16 = mp.get("bf16_tflops_sustained") or mp.get("bf16_tflops")
+        tf32_peak = (bf16 / 2.0) if bf16 else 1100.0
+        tr = _load_traffic("tc_scan_traffic.json")
+        mma_tflops = tc_items * 2.0 * 128 * 128 * 32 / (scan_ms / 1e3) / 1e12
+        roofline = {
+            "bound": "tensor", "achieved": alg_tflops, "peak": tf32_peak, "unit": "TFLOP/s",
+            "frac": alg_tflops / tf32_peak,
+            "traffic": (tr["dram_bytes_per_item"] * tc_items / max(scans, 1)) if tr else None,
+            "traffic_note": "dram bytes per launch = ncu dram__bytes_read+write per tile-pair item "
+                            "(profiles/tc_scan_traffic.json) x average items per launch",
+            "kernel": "tc_scan_kernel (tcgen05 kind::tf32 128x128x32 MMA per tile pair, TMEM "
+                      "accumulators; fused centring, component masks, threshold filter, exact-key "
+                      "top-2)",
+            "peak_source": ("dense TF32 = 1/2 of MEASURED_PEAKS.json bf16_tflops_sustained "
+                            f"({bf16} TF/s)" if bf16 else "B200_PROFILING.md fallback 1.1 PF/s tf32"),
+            "mma_tflops": mma_tflops, "mma_frac": mma_tflops / tf32_peak,
+            "fp32_roofline_frac": alg_tflops / peak.value if peak.value else None,
+            "fp32_peak": peak.value,
+            "fp32_peak_source": "measured FFMA2 microbenchmark on this GPU (nnm_measure_fp32_peak)",
+            "avg_launch_ms": avg_launch_ms, "launches": scans, "tc_items": tc_items,
+            "scan_share_of_step": scan_ms / (ms_dev * args.steps)}
+    else:
+        tr = _load_traffic("scan_traffic.json")
+        bpp = tr.get("dram_bytes_per_pair") if tr else None
+        roofline = {"bound": "fp32", "achieved": alg_tflops, "peak": peak.value, "unit": "TFLOP/s",
+                    "frac": alg_tflops / peak.value if peak.value else None,
+                    "traffic": (bpp * pairs_eval / max(scans, 1)) if bpp is not None else None,
+                    "traffic_note": "dram bytes per launch = ncu dram__bytes_read+write per pair "
+                                    "(profiles/scan_traffic.json) x average pairs per launch",
+                    "kernel": "scan_reg_kernel (fused FP32 dot-form distance + eligibility + per-row "
+                              "top-2 threshold filter)",
+                    "peak_source": "measured FFMA2 microbenchmark on this GPU (MEASURED_PEAKS.json "
+                                   "has no FP32 entry)",
+                    "avg_launch_ms": avg_launch_ms, "launches": scans,
+                    "scan_share_of_step": scan_ms / (ms_dev * args.steps)}
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -312,7 +349,8 @@ def run_gpu(args) -> None:
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "fp32-screen+f64-exact",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": ("tf32-tensor-screen+f64-exact" if tc_items > 0 else "fp32-screen+f64-exact"),
         "data": "synthetic (generate_synthetic, bit-identical to the reference generator)",
         "config": cfg, "e2e": e2e, "roofline": roofline, "cpu_baseline": cb,
         "clocks": clocks, "gpu_launches": launches,
