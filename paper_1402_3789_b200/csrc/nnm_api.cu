@@ -58,8 +58,13 @@ struct NnmError {
 
 [[noreturn]] void invalid(const std::string& m) { throw NnmError{NNM_E_INVALID, m}; }
 
+thread_local cudaStream_t t_alloc_stream = nullptr;  // stream for DevBuf allocations
+
 template <class F>
 int guarded(F&& f) {
+  // every entry point starts on the default stream; dataset entry points then select the
+  // dataset's own stream (a stale stream of a destroyed dataset must never be reused)
+  t_alloc_stream = nullptr;
   try {
     f();
     return NNM_OK;
@@ -76,7 +81,6 @@ int guarded(F&& f) {
 // stream of the dataset being worked on, with the pool's release threshold
 // raised: repeated dataset create / destroy (one per user call through the
 // reference-facing API) then costs no cudaMalloc / device-wide cudaFree syncs.
-thread_local cudaStream_t t_alloc_stream = nullptr;
 
 template <class T>
 struct DevBuf {
@@ -570,6 +574,20 @@ __device__ __forceinline__ float cdist32(const float* __restrict__ c32, int T, c
   return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? sqrtf(acc) : acc;
 }
 
+// as cdist32 with the row centre read strided from the SoA array (ci[k * T])
+template <int M>
+__device__ __forceinline__ float cdist32s(const float* __restrict__ c32, int T, const float* ci, int J,
+                                          int d) {
+  float acc = 0.f;
+  for (int k = 0; k < d; ++k) {
+    const float t = fabsf(__ldg(ci + (int64_t)k * T) - __ldg(c32 + (int64_t)k * T + J));
+    if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc = fmaf(t, t, acc);
+    else if (M == MANHATTAN) acc += t;
+    else acc = fmaxf(acc, t);
+  }
+  return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? sqrtf(acc) : acc;
+}
+
 // rigorous lower bound (internal units) of every pair of tile pair (I, J) from the fp32
 // centre distance: fp32 evaluation error <= (d+4)u dc, centre rounding <= u (|c_I|+|c_J|)
 template <int M>
@@ -579,6 +597,41 @@ __device__ __forceinline__ double tile_lb32(float dc, float cnI, float cnJ, floa
   const double r = lo * (1.0 - 1e-9) - (double)rI - (double)rJ;
   if (!(r > 0.0)) return 0.0;
   return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? r * r * (1.0 - 1e-9) : r * (1.0 - 1e-9);
+}
+
+// Full-square item list for the tensor-core scan: out[2w] = (I, J), out[2w+1] = (J, I);
+// the diagonal twin and (with umax) every orientation whose rigorous tile lower bound
+// exceeds the row tile's component bound become the sentinel (INT_MAX, INT_MAX).
+__global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n,
+                                 const double* __restrict__ umax, const float* __restrict__ c32,
+                                 const float* __restrict__ cn, const float* __restrict__ r32, int T,
+                                 int d, int metric, int2* __restrict__ out,
+                                 unsigned long long* __restrict__ dropped) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned drop = 0;
+  if (w < n) {
+    const int2 it = items[w];
+    const int2 none = make_int2(0x7FFFFFFF, 0x7FFFFFFF);
+    bool keep_ij = true, keep_ji = it.x != it.y;
+    if (umax && it.x != it.y) {
+      // same fp32 centre distance and bound as enum_count_kernel (the item passed it)
+      const float* ci = c32 + it.x;  // strided view: ci[k * T] is coordinate k of tile I
+      double lb;
+      if (metric == MANHATTAN)
+        lb = tile_lb32<MANHATTAN>(cdist32s<MANHATTAN>(c32, T, ci, it.y, d), cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
+      else if (metric == CHEBYSHEV)
+        lb = tile_lb32<CHEBYSHEV>(cdist32s<CHEBYSHEV>(c32, T, ci, it.y, d), cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
+      else
+        lb = tile_lb32<EUCLIDEAN>(cdist32s<EUCLIDEAN>(c32, T, ci, it.y, d), cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
+      keep_ij = lb <= umax[it.x];
+      keep_ji = lb <= umax[it.y];
+    }
+    out[2 * w] = keep_ij ? it : none;
+    out[2 * w + 1] = keep_ji ? make_int2(it.y, it.x) : none;
+    drop = (keep_ij ? 0u : 1u) + (keep_ji ? 0u : 1u);
+  }
+  drop = __reduce_add_sync(0xFFFFFFFFu, drop);
+  if ((threadIdx.x & 31) == 0 && drop) atomicAdd(dropped, (unsigned long long)drop);
 }
 
 // Phase 1: for each tile I the PK tile pairs with the smallest LB among tiles
@@ -1210,7 +1263,7 @@ struct nnm_dataset {
   // tensor-core scan (Euclidean Boruvka, d <= TC_MAX_D; nnm_tc.cu)
   bool tc_on = false;
   bool tc_ready = false;
-  DevBuf<float> tc_img, tc_tnorm, tc_eta, tc_meta;
+  DevBuf<float> tc_img, tc_tnorm, tc_eta, tc_meta, tc_sq;
   DevBuf<int2> tc_items;
   // dot form
   bool dot_on = false;
@@ -1320,14 +1373,14 @@ struct nnm_dataset {
   // full or partial screening scan into (b1, b2); times the launch with events
   void scan(int metric, unsigned long long* b1, unsigned long long* b2, bool top2, int kl2, int kl3,
             float thr_hi, int64_t w_begin, int64_t w_end, const int2* items = nullptr,
-            bool reset = true) {
+            bool reset = true, const double* orient_umax = nullptr) {
     if (reset) {
       fill_none(b1, vn);
       if (b2) fill_none(b2, vn);
     }
     if (tc_on && items && b2 && top2 && cur_X32 == X32p.p && kl2 == INT_UNSET &&
         kl3 == INT_UNSET) {
-      tc_scan(b1, b2, thr_hi, w_begin, w_end, items);
+      tc_scan(b1, b2, thr_hi, w_begin, w_end, items, orient_umax);
       return;
     }
     tile_range.ensure(vT);
@@ -1390,8 +1443,9 @@ struct nnm_dataset {
     tc_tnorm.ensure(np_);
     tc_eta.ensure(np_);
     tc_meta.ensure((size_t)Tp * TC_META);
+    tc_sq.ensure(np_);
     CUDA_TRY(launch_tc_prepare(X64p.p, porig.p, tcenter.p, normp.p, np_, d, Tp, tc_img.p,
-                               tc_tnorm.p, tc_eta.p, tc_meta.p, st));
+                               tc_tnorm.p, tc_eta.p, tc_meta.p, tc_sq.p, st));
     note_launch();
     note_launch();
     tc_ready = true;
@@ -1399,26 +1453,31 @@ struct nnm_dataset {
 
   // tensor-core screening scan of the listed (upper-triangular) tile pairs: the list
   // is mirrored to the full square and sorted by row tile, then scanned row-wise
+  // umax (phase 2 only): an orientation (I, J) serves the rows of tile I alone, so it is
+  // dropped when the tile pair's rigorous lower bound exceeds UMAX_I (DESIGN 3.1)
   void tc_scan(unsigned long long* b1, unsigned long long* b2, float thr_hi, int64_t w_begin,
-               int64_t w_end, const int2* items) {
+               int64_t w_end, const int2* items, const double* umax = nullptr) {
     const int64_t n_up = w_end - w_begin;
     if (n_up <= 0) return;
     tc_prepare();
     tc_items.ensure((size_t)2 * n_up);
-    CUDA_TRY(launch_tc_mirror(items + w_begin, n_up, tc_items.p, st));
-    note_launch();
-    auto* k64 = reinterpret_cast<unsigned long long*>(tc_items.p);
-    thrust::sort(thrust::cuda::par(talloc).on(st), k64, k64 + 2 * n_up, ItemLess());
-    // diagonal items left a sentinel each (sorted last): count the real ones
     counters.ensure(8);
     CUDA_TRY(cudaMemsetAsync(counters.p + 5, 0, sizeof(unsigned long long), st));
-    count_diag_kernel<<<blocks_for(n_up), 256, 0, st>>>(items + w_begin, n_up, counters.p + 5); note_launch();
+    // every dropped orientation / diagonal twin leaves a sentinel (sorted last), counted
+    tc_mirror_kernel<<<blocks_for(n_up), 256, 0, st>>>(items + w_begin, n_up, umax, tc32.p, tcn32.p,
+                                                       tr32.p, Tp, d, bv_metric, tc_items.p,
+                                                       counters.p + 5); note_launch();
+    CUDA_TRY(cudaGetLastError());
+    auto* k64 = reinterpret_cast<unsigned long long*>(tc_items.p);
+    thrust::sort(thrust::cuda::par(talloc).on(st), k64, k64 + 2 * n_up, ItemLess());
     const int64_t nfull = 2 * n_up - (int64_t)read1(counters.p + 5);
+    if (nfull <= 0) return;
     TcArgs a;
     a.img = tc_img.p;
     a.tnorm = tc_tnorm.p;
     a.eta = tc_eta.p;
     a.meta = tc_meta.p;
+    a.sq = tc_sq.p;
     a.comp = comp.p;
     a.X64 = X64p.p;
     a.np = (int)np_;
@@ -1806,7 +1865,8 @@ struct nnm_dataset {
       default: ucomp_t<EUCLIDEAN>(b1); pruned_phase2<EUCLIDEAN>(n2);
     }
     const int64_t lo2 = n2 * rank / world, hi2 = n2 * (rank + 1) / world;
-    if (hi2 > lo2) scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, lo2, hi2, items2.p, false);
+    if (hi2 > lo2)
+      scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, lo2, hi2, items2.p, false, tumax.p);
     if (rank == 0) pairs_covered += (double)n * (double)(n - 1) / 2.0;
     if (getenv("NNM_DEBUG")) {
       const int T = Tp;
@@ -2495,6 +2555,7 @@ int nnm_tc_probe(nnm_dataset* ds, const int32_t* items, int64_t n_items, double*
     a.tnorm = ds->tc_tnorm.p;
     a.eta = ds->tc_eta.p;
     a.meta = ds->tc_meta.p;
+    a.sq = ds->tc_sq.p;
     a.comp = ds->comp.p;
     a.X64 = ds->X64p.p;
     a.np = (int)ds->np_;

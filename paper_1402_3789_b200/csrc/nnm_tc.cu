@@ -70,8 +70,11 @@ struct TcSmem {
   float metaB[TC_STAGES][TC_META];
   int acomp[2][TILE];                  // component labels of the row / column tiles
   int bcomp[TC_STAGES][TILE];
-  float rrow[TC_STAGES][TILE];         // r_i of each row for the item in the stage
-  float dn[TC_STAGES];                 // |D| of the item
+  float asq[2][TILE];                  // |x_t|^2 of the row tile's positions
+  float bsq[TC_STAGES][TILE];          // |y_t|^2 of the column tile's positions
+  float rrow[TC_STAGES][TILE];         // per row of the item: r_i, E and eta (prep -> epilogue)
+  float erow[TC_STAGES][TILE];
+  float etarow[TC_STAGES][TILE];
   int2 ring[TC_RING];                  // (I, J) of item q at q % TC_RING (written by the producer)
   int slot[2][8];
   int slotcnt[TC_PREP_GROUPS][4];  // first-occurrence counts per 32-row block
@@ -204,6 +207,14 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
 __device__ __forceinline__ void trace(const TcArgs& p, int role, int q, int ev) {
   if (p.trace && blockIdx.x == 0 && q < 256) p.trace[(role * 256 + q) * 2 + ev] = clock64();
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
   uint32_t r;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
@@ -273,45 +284,51 @@ __device__ __forceinline__ uint32_t slot_hits(int comp, const int (&slot)[8]) {
   return h;
 }
 
-// One pass over the coordinates of an item for one row / column position:
-//   D = c_J - c_I (fp32), s = |y_t|^2 + 2 D.y_t, r = |x_t - D|^2, |D|
-// (independent partial sums per lane of a 4-chunk: any summation order is inside the
-// error bound).  Shared by the prep warps and the probe so both round identically.
-__device__ __forceinline__ void tc_item_sums(const float* __restrict__ mj, const float* __restrict__ mi,
-                                             const float* __restrict__ yrow_tile, int yr,
-                                             const float (&x)[32], int d, float& s_out,
-                                             float& r_out, float& dn_out) {
-  float s4[4] = {0.f, 0.f, 0.f, 0.f}, r4[4] = {0.f, 0.f, 0.f, 0.f}, n4[4] = {0.f, 0.f, 0.f, 0.f};
+// Per-item quantities (shared by the prep warps and the probe so both round
+// identically; any summation order is inside the error bound):
+//   D = c_J - c_I (fp32), |D|^2, r_i = |x_t|^2 - 2 x_t.D + |D|^2, s_j = |y_t|^2 + 2 D.y_t
+// with |x_t|^2 / |y_t|^2 precomputed per position (tc_prepare_kernel).
+__device__ __forceinline__ float tc_delta(const float* __restrict__ mj, const float* __restrict__ mi,
+                                          int d, float (&dl)[32]) {
+  float n2[2] = {0.f, 0.f};
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    if (4 * c >= d) continue;
+    if (4 * c >= d) {
+      dl[4 * c] = dl[4 * c + 1] = dl[4 * c + 2] = dl[4 * c + 3] = 0.f;
+      continue;
+    }
     const float4 a = *reinterpret_cast<const float4*>(mj + 4 * c);
     const float4 b = *reinterpret_cast<const float4*>(mi + 4 * c);
-    const float4 y = *reinterpret_cast<const float4*>(yrow_tile + swz(yr, c));
-    const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-    const float yv[4] = {y.x, y.y, y.z, y.w};
+    dl[4 * c] = a.x - b.x; dl[4 * c + 1] = a.y - b.y; dl[4 * c + 2] = a.z - b.z; dl[4 * c + 3] = a.w - b.w;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (4 * c + u >= d) continue;
-      const float dl = av[u] - bv[u];
-      s4[u] = fmaf(yv[u], yv[u] + 2.f * dl, s4[u]);
-      const float e = x[4 * c + u] - dl;
-      r4[u] = fmaf(e, e, r4[u]);
-      n4[u] = fmaf(dl, dl, n4[u]);
-    }
+    for (int u = 0; u < 4; ++u)
+      if (4 * c + u < d) n2[u & 1] = fmaf(dl[4 * c + u], dl[4 * c + u], n2[u & 1]);
   }
-  s_out = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-  r_out = (r4[0] + r4[1]) + (r4[2] + r4[3]);
-  dn_out = sqrtf((n4[0] + n4[1]) + (n4[2] + n4[3])) * 1.000001f;
+  return n2[0] + n2[1];
+}
+__device__ __forceinline__ float tc_dot(const float (&x)[32], const float (&dl)[32], int d) {
+  float q4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k < d) q4[k & 3] = fmaf(x[k], dl[k], q4[k & 3]);
+  return (q4[0] + q4[1]) + (q4[2] + q4[3]);
+}
+__device__ __forceinline__ float tc_r(float xsq, float q, float dn2) {
+  return __fmaf_rn(-2.f, q, xsq) + dn2;
+}
+__device__ __forceinline__ float tc_dnorm(float dn2, int d) {
+  return sqrtf(dn2) * (1.0f + (d + 4) * TC_U * 2.f);
 }
 
 // Squared-domain evaluation bound E of a row's pairs with tile J (all terms but the |v|
 // one, which lower_key adds) and the distance-domain rounding bound eta (file header).
-// sb bounds |s_j| = ||y_t|^2 + 2 D.y_t| through the tile radius RJ.
-__device__ __forceinline__ void tc_bounds(float r, float dnorm, int d, float tn_i, float eta_i,
-                                          float RJ, float etaJ, float& Erow, float& eta_row) {
+// r error <= (d+3) u (|x_t| + |D|)^2, s error <= (d+3) u (|y_t|^2 + 2 |y_t||D|) with
+// sb = RJ (RJ + 2|D|) >= |s_j|, split 2^-22 |s|, tensor-core accumulation.
+__device__ __forceinline__ void tc_bounds(float dnorm, int d, float tn_i, float eta_i, float RJ,
+                                          float etaJ, float& Erow, float& eta_row) {
   const float sb = RJ * (RJ + 2.f * dnorm);
-  Erow = ((d + 3) * TC_U * 1.02f * r + (d + 2) * TC_U * 1.01f * sb + 2.4e-7f * sb +
+  const float xr = tn_i + dnorm;
+  Erow = ((d + 3) * TC_U * 1.02f * xr * xr + (d + 3) * TC_U * 1.01f * sb + 2.4e-7f * sb +
           2.f * TC_CACC * (tn_i * RJ + 0.51f * sb)) * 1.01f + 1e-30f;
   eta_row = (eta_i + etaJ + TC_U * 1.001f * dnorm) * 1.0001f;
 }
@@ -424,19 +441,21 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
           prevI = it.x;
           const int xb = rt & 1;
           if (rt >= 2) mbar_wait(&S.aempty[xb], ((rt - 2) >> 1) & 1);
-          mbar_expect_tx(&S.afull[xb], TC_TILE_BYTES + TC_META * 4 + TILE * 4);
+          mbar_expect_tx(&S.afull[xb], TC_TILE_BYTES + TC_META * 4 + 2 * TILE * 4);
           bulk_g2s(S.A[xb], p.img + (int64_t)it.x * TC_TILE_FLOATS, TC_TILE_BYTES, &S.afull[xb]);
           bulk_g2s(S.metaA[xb], p.meta + (int64_t)it.x * TC_META, TC_META * 4, &S.afull[xb]);
           bulk_g2s(S.acomp[xb], p.comp + (int64_t)it.x * TILE, TILE * 4, &S.afull[xb]);
+          bulk_g2s(S.asq[xb], p.sq + (int64_t)it.x * TILE, TILE * 4, &S.afull[xb]);
         }
         const int s = q % TC_STAGES;
         if (q >= TC_STAGES) mbar_wait(&S.empty[s], ((q / TC_STAGES) - 1) & 1);
         trace(p, 0, q, 0);
         S.ring[q % TC_RING] = it;  // published to the other roles by the full barrier
-        mbar_expect_tx(&S.full[s], TC_TILE_BYTES + TC_META * 4 + TILE * 4);
+        mbar_expect_tx(&S.full[s], TC_TILE_BYTES + TC_META * 4 + 2 * TILE * 4);
         bulk_g2s(S.B[s], p.img + (int64_t)it.y * TC_TILE_FLOATS, TC_TILE_BYTES, &S.full[s]);
         bulk_g2s(S.metaB[s], p.meta + (int64_t)it.y * TC_META, TC_META * 4, &S.full[s]);
         bulk_g2s(S.bcomp[s], p.comp + (int64_t)it.y * TILE, TILE * 4, &S.full[s]);
+        bulk_g2s(S.bsq[s], p.sq + (int64_t)it.y * TILE, TILE * 4, &S.full[s]);
       }
     }
   } else if (warp == TC_MMA_WARP) {
@@ -477,6 +496,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
     const int pt = tid - TC_EPI_WARPS * 32 - g * TC_PREP_THREADS;
     int rt = -1, myI = -1;
     float xa[32], xb2[32];
+    float tna = 0.f, tnb = 0.f, eta_a = 0.f, eta_b = 0.f;
     int slot[8];
     for (int q = g; q < nq; q += TC_PREP_GROUPS) {
       const int s = q % TC_STAGES;
@@ -495,6 +515,10 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
       const int xb = rt & 1;
       if (I != myI) {
         myI = I;
+        tna = __ldg(p.tnorm + (int64_t)I * TILE + pt);
+        tnb = __ldg(p.tnorm + (int64_t)I * TILE + pt + 64);
+        eta_a = __ldg(p.eta + (int64_t)I * TILE + pt);
+        eta_b = __ldg(p.eta + (int64_t)I * TILE + pt + 64);
         if (I != Im1) {
           // first item of the row tile: this group prepares the A operand
           mbar_wait(&S.afull[xb], (rt >> 1) & 1);
@@ -525,17 +549,28 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         continue;
       }
       if (pt == 0) trace(p, 5, q, 0);
-      float sa, ra, dn, sb, rb, dn2;
-      tc_item_sums(S.metaB[s], S.metaA[xb], S.B[s], pt, xa, d, sa, ra, dn);
-      tc_item_sums(S.metaB[s], S.metaA[xb], S.B[s], pt + 64, xb2, d, sb, rb, dn2);
-      if (pt == 0) trace(p, 5, q, 1);
+      float dl[32];
+      const float dn2 = tc_delta(S.metaB[s], S.metaA[xb], d, dl);
+      const float dnorm = tc_dnorm(dn2, d);
+      const float RJ = S.metaB[s][32], etaJ = S.metaB[s][33];
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        const int col = pt + 64 * half;
-        const float sj = half ? sb : sa;
+        // row pt + 64 half: r_i and its bounds for the epilogue
+        const int row = pt + 64 * half;
+        const float r = tc_r(S.asq[xb][row], tc_dot(half ? xb2 : xa, dl, d), dn2);
+        float Erow, eta_row;
+        tc_bounds(dnorm, d, half ? tnb : tna, half ? eta_b : eta_a, RJ, etaJ, Erow, eta_row);
+        S.rrow[s][row] = r;
+        S.erow[s][row] = Erow;
+        S.etarow[s][row] = eta_row;
+        // column pt + 64 half: s_j = |y|^2 + 2 D.y into the K tail (hi / lo), slot hits
+        const int col = row;
+        float y[32];
+        load_row(S.B[s], col, d, y);
         const int cj = S.bcomp[s][col];
         float hi, lo;
         if (cj >= 0) {
+          const float sj = __fmaf_rn(2.f, tc_dot(y, dl, d), S.bsq[s][col]);
           const float hh = -0.5f * sj;
           hi = tf32_rna(hh);
           lo = tf32_rna(hh - hi);
@@ -545,9 +580,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         }
         write_tail(S.B[s], col, d, kc, hi, lo, slot_hits(cj, slot), 1.f);
       }
-      S.rrow[s][pt] = ra;
-      S.rrow[s][pt + 64] = rb;
-      if (pt == 0) S.dn[s] = dn;
+      if (pt == 0) trace(p, 5, q, 1);
       if (!(p.dbg & 4)) fence_proxy_async();  // (dbg 4: timing experiment only)
       if (pt == 0) trace(p, 7, q, 0);
       group_bar(g);
@@ -566,7 +599,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
     const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     int prevI = -1;
     unsigned long long k1 = NONE_KEY, k2 = NONE_KEY;
-    float tn_i = 0.f, eta_i = 0.f, gT = INFINITY;
+    float gT = INFINITY;
     int ci = -1;
     int64_t g = 0;
     for (int q = e; q < nq; q += TC_EPI_GROUPS) {
@@ -581,15 +614,11 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         prevI = I;
         g = (int64_t)I * TILE + i;
         ci = __ldg(p.comp + g);
-        tn_i = __ldg(p.tnorm + g);
-        eta_i = __ldg(p.eta + g);
         const unsigned long long gb = *((volatile const unsigned long long*)(p.B2 + g));
         gT = key_valid(gb) ? key_value(gb) : INFINITY;
         k1 = k2 = NONE_KEY;
       }
-      const float r = S.rrow[s][i];
-      float Erow, eta_row;
-      tc_bounds(r, S.dn[s], d, tn_i, eta_i, S.metaB[s][32], S.metaB[s][33], Erow, eta_row);
+      const float r = S.rrow[s][i], Erow = S.erow[s][i], eta_row = S.etarow[s][i];
       // G' threshold equivalent to "L <= T may hold" (vthr: largest v with L <= T)
       auto gamma_of = [&](float T) -> float {
         if (!(T < INFINITY)) return -INFINITY;
@@ -604,7 +633,9 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
       if (tid == 0) trace(p, 3, q, 0);
       tc_after();
       if (!(p.dbg & 1)) {
-        bool want = false;
+        // fast filter, 64 columns at a time: maxima of the 8-column groups (the first
+        // levels of the reduction tree) -> bit mask of groups that may hold a candidate
+        uint32_t gm = 0;
 #pragma unroll 1
         for (int hb = 0; hb < 2; ++hb) {
           float v[64];
@@ -614,26 +645,38 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
 #pragma unroll
             for (int jj = 0; jj < 64; ++jj) o[jj] = v[jj];
           } else {
-            want |= fmaxf(max32(v), max32(v + 32)) >= gam;
+            float g8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              g8[k] = fmaxf(fmaxf(fmaxf(v[8 * k], v[8 * k + 1]), fmaxf(v[8 * k + 2], v[8 * k + 3])),
+                            fmaxf(fmaxf(v[8 * k + 4], v[8 * k + 5]), fmaxf(v[8 * k + 6], v[8 * k + 7])));
+            uint32_t m = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) m |= (g8[k] >= gam) ? (1u << k) : 0u;
+            gm |= (ci >= 0 ? m : 0u) << (8 * hb);
           }
         }
-        if (!p.dump && __any_sync(0xFFFFFFFFu, ci >= 0 && want)) {
-          // exact insert path (rare): re-read this row's values one by one (a rolled
-          // loop keeps the code small); a pair whose screened lower bound can beat the
-          // row's second best gets its exact scipy-order FP64 value (rounded down) as key,
-          // so certification in refine is as sharp as the FP64 order allows
-          // (tcgen05.ld is warp-collective: every lane loads, each lane filters its own row)
+        // exact insert path (rare): the warp re-reads only the 8-column groups where some
+        // lane may hold a candidate (tcgen05.ld is warp-collective); each lane re-filters
+        // its row with its current threshold, and a pair that can enter the top-2 gets its
+        // exact scipy-order FP64 value (rounded down) as key
+        uint32_t wm = __reduce_or_sync(0xFFFFFFFFu, gm);
 #pragma unroll 1
-          for (int j = 0; j < TILE; ++j) {
-            __syncwarp();
-            const float vj = tmem_ld1(lane_base + a * TILE + j);
-            if (ci < 0 || !(vj >= gam)) continue;
+        while (wm) {
+          const int gidx = __ffs(wm) - 1;
+          wm &= wm - 1;
+          float w[8];
+          tmem_ld8(lane_base + a * TILE + gidx * 8, w);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (ci < 0 || !(w[u] >= gam)) continue;
+            const int j = gidx * 8 + u;
             const int cj = S.bcomp[s][j];
             if (cj < 0 || cj == ci) continue;
-            if (!(lower_key(__fmaf_rn(-2.f, vj, r), Erow, eta_row) <= T)) continue;
+            if (!(lower_key(__fmaf_rn(-2.f, w[u], r), Erow, eta_row) <= T)) continue;
             const int64_t gj = (int64_t)J * TILE + j;
             const float L = float_down(exact_dist<EUCLIDEAN>(p.X64 + g * d, p.X64 + gj * d, d));
-            if (!(L <= p.thr_hi)) continue;
+            if (!(L <= T)) continue;  // cannot enter the top-2 (T: second best, global, dmax)
             const unsigned long long key = ((unsigned long long)__float_as_uint(L) << 32) | (unsigned)gj;
             if (key < k2) {
               if (key < k1) {
@@ -671,7 +714,8 @@ __global__ void tc_prepare_kernel(const double* __restrict__ X64p, const int* __
                                   const double* __restrict__ tcenter64,
                                   const double* __restrict__ normp, int64_t np, int d,
                                   float* __restrict__ img, float* __restrict__ tnorm,
-                                  float* __restrict__ eta, float* __restrict__ meta) {
+                                  float* __restrict__ eta, float* __restrict__ meta,
+                                  float* __restrict__ sq) {
   const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pos >= np) return;
   const int64_t T0 = pos / TILE;
@@ -697,10 +741,16 @@ __global__ void tc_prepare_kernel(const double* __restrict__ X64p, const int* __
     }
     const double u = 5.9604644775390625e-08;
     tnorm[pos] = float_up(sqrt(tn2) * (1.0 + 1e-12));
+    float q = 0.f;  // |x_t|^2 as an fp32 FMA chain (inside the (d+3) u (|x_t| + |D|)^2 term)
+#pragma unroll
+    for (int k = 0; k < TC_K; ++k)
+      if (k < d) q = fmaf(xt[k], xt[k], q);
+    sq[pos] = q;
     eta[pos] = float_up((u * normp[pos] + (1.001 * u + 4.8828125e-04) * sqrt(xc2)) * 1.0001 + 1e-30);
   } else {
     tnorm[pos] = 0.f;
     eta[pos] = 0.f;
+    sq[pos] = 0.f;
   }
   float* o = img + T0 * TC_TILE_FLOATS;
 #pragma unroll
@@ -751,13 +801,12 @@ __global__ void tc_probe_kernel(TcArgs p, const double* __restrict__ X64p, const
   const int I = it.x, J = it.y, d = p.d;
   const int64_t gi = (int64_t)I * TILE + i;
   if (p.comp[gi] < 0) return;
-  float x[32];
+  float x[32], dl[32];
   load_row(p.img + (int64_t)I * TC_TILE_FLOATS, i, d, x);
-  float sj, r, dnorm;  // (sj unused: the column term is inside the dumped accumulator)
-  tc_item_sums(p.meta + (int64_t)J * TC_META, p.meta + (int64_t)I * TC_META,
-               p.img + (int64_t)J * TC_TILE_FLOATS, i, x, d, sj, r, dnorm);
+  const float dn2 = tc_delta(p.meta + (int64_t)J * TC_META, p.meta + (int64_t)I * TC_META, d, dl);
+  const float r = tc_r(p.sq[gi], tc_dot(x, dl, d), dn2);
   float Erow, eta_row;
-  tc_bounds(r, dnorm, d, p.tnorm[gi], p.eta[gi], p.meta[(int64_t)J * TC_META + 32],
+  tc_bounds(tc_dnorm(dn2, d), d, p.tnorm[gi], p.eta[gi], p.meta[(int64_t)J * TC_META + 32],
             p.meta[(int64_t)J * TC_META + 33], Erow, eta_row);
   float worst = 0.f;
   unsigned long long bad = 0, cnt = 0;
@@ -826,9 +875,9 @@ cudaError_t launch_tc_scan(const TcArgs& a, int grid, cudaStream_t st) {
 
 cudaError_t launch_tc_prepare(const double* X64p, const int* porig, const double* tcenter64,
                               const double* normp, int64_t np, int d, int T, float* img,
-                              float* tnorm, float* eta, float* meta, cudaStream_t st) {
+                              float* tnorm, float* eta, float* meta, float* sq, cudaStream_t st) {
   tc_prepare_kernel<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(X64p, porig, tcenter64, normp, np,
-                                                                  d, img, tnorm, eta, meta);
+                                                                  d, img, tnorm, eta, meta, sq);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   tc_tile_max_kernel<<<T, TILE, 0, st>>>(tnorm, eta, meta);

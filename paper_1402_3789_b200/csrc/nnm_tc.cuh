@@ -17,6 +17,7 @@ struct TcArgs {
   const float* img;       // [T][128][32] swizzled operand image: tf32-exact centred coords, 0 elsewhere
   const float* tnorm;     // [np] |x_t| of each position, rounded up (0 for pads)
   const float* eta;       // [np] distance-domain rounding bound of each position, rounded up
+  const float* sq;        // [np] |x_t|^2 of each position (fp32 FMA chain)
   const float* meta;      // [T][TC_META] tile records: fp32 centre the image was centred on
                           // (32, zero padded), max tnorm (32), max eta (33)
   const int* comp;        // [np] component label per position (-1: pad)
@@ -39,7 +40,7 @@ cudaError_t launch_tc_scan(const TcArgs& a, int grid, cudaStream_t st);
 // Operand image + per-position / per-tile bounds for the kd view (once per dataset).
 cudaError_t launch_tc_prepare(const double* X64p, const int* porig, const double* tcenter64,
                               const double* normp, int64_t np, int d, int T, float* img,
-                              float* tnorm, float* eta, float* meta, cudaStream_t st);
+                              float* tnorm, float* eta, float* meta, float* sq, cudaStream_t st);
 
 // Error-model probe over dumped accumulators (a.dump filled by launch_tc_scan for `items`).
 cudaError_t launch_tc_probe(const TcArgs& a, const double* X64p, const int2* items, int64_t n,
