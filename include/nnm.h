@@ -158,6 +158,20 @@ int nnm_bv_finish_round(nnm_dataset *ds, const uint64_t *B1_dev, const uint64_t 
 int nnm_bv_end(nnm_dataset *ds, int64_t kl1, nnm_merge *out_merges, int64_t *out_n_merges,
                int64_t *out_assign, int64_t *out_rounds, int32_t *out_stop, nnm_stats *stats);
 
+/* ---- CSV ingestion (dataio.py:49-116 load_dataset) ----
+ * Parses a delimited text file with the reference's exact rules and messages:
+ * str.splitlines() line boundaries, blank lines skipped, header sniffed (any field
+ * not a Python float()), id column by header name or 0-based index, Python float()
+ * grammar (underscores, inf/nan), errors cite 1-based physical lines (NNM_E_INVALID,
+ * message in nnm_last_error()).  Multi-threaded; threads <= 0 uses every core.
+ * nnm_csv_fetch copies the n x d row-major values and, with ids, the concatenated
+ * UTF-8 ids plus n+1 offsets (*id_bytes total).  No GPU involved. */
+typedef struct nnm_csv nnm_csv;
+int nnm_csv_load(const char *path, char delimiter, const char *id_column, int32_t threads,
+                 nnm_csv **out, int64_t *n, int64_t *d, int32_t *has_ids, int64_t *id_bytes);
+int nnm_csv_fetch(nnm_csv *table, double *values, char *id_buf, int64_t *id_offsets);
+int nnm_csv_free(nnm_csv *table);
+
 /* ---- diagnostics ----
  * Sustained FP32 (FFMA2) throughput of `device` in TFLOP/s: the roofline
  * denominator for the screening scan, which runs on the FP32 pipe. */

@@ -35,7 +35,8 @@ EXPORTED = (
     "nnm_abi_version", "nnm_last_error", "nnm_device_count", "nnm_dataset_create",
     "nnm_dataset_create_device", "nnm_dataset_destroy", "nnm_top_p", "nnm_run",
     "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_scan_pruned", "nnm_bv_second", "nnm_bv_finish_round",
-    "nnm_bv_end", "nnm_measure_fp32_peak", "nnm_tc_probe",
+    "nnm_bv_end", "nnm_measure_fp32_peak", "nnm_tc_probe", "nnm_csv_load", "nnm_csv_fetch",
+    "nnm_csv_free",
 )
 
 
@@ -107,6 +108,10 @@ def load():
         lib.nnm_bv_scan.argtypes = [vp, i64, i64, vp, vp]
         lib.nnm_bv_scan_pruned.argtypes = [vp, i32, i32, vp, vp]
         lib.nnm_tc_probe.argtypes = [vp, vp, i64, P(dbl)]
+        lib.nnm_csv_load.argtypes = [ctypes.c_char_p, ctypes.c_char, ctypes.c_char_p, i32, P(vp),
+                                     P(i64), P(i64), P(i32), P(i64)]
+        lib.nnm_csv_fetch.argtypes = [vp, vp, vp, vp]
+        lib.nnm_csv_free.argtypes = [vp]
         lib.nnm_bv_second.argtypes = [vp, vp, vp, vp, vp]
         lib.nnm_bv_finish_round.argtypes = [vp, vp, vp, P(i64)]
         lib.nnm_bv_end.argtypes = [vp, i64, vp, P(i64), vp, P(i64), P(i32), P(Stats)]
@@ -170,3 +175,32 @@ def device_dataset(dataset) -> DeviceDataset:
         dd = DeviceDataset(dataset.values, device=dev)
         object.__setattr__(dataset, "_device_cache", dd)
     return dd
+
+
+def load_csv(path: str, *, delimiter: str = ",", id_column=None, threads: int = 0):
+    """Native CSV ingestion (nnm_csv_load): returns (values float64 (n, d), ids list or None).
+    Raises ValidationError with the reference's messages (dataio.py:49-116)."""
+    lib = load()
+    if len(delimiter.encode("utf-8")) != 1:
+        raise NotImplementedError("native CSV ingestion needs a single-byte delimiter")
+    h = ctypes.c_void_p()
+    n, d, nid = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    has = ctypes.c_int32()
+    idc = None if id_column is None else str(id_column).encode("utf-8")
+    check(lib.nnm_csv_load(os.fsencode(path), delimiter.encode("utf-8"), idc, int(threads),
+                           ctypes.byref(h), ctypes.byref(n), ctypes.byref(d), ctypes.byref(has),
+                           ctypes.byref(nid)))
+    try:
+        values = np.empty((n.value, d.value), dtype=np.float64)
+        ids = None
+        if has.value:
+            buf = ctypes.create_string_buffer(max(1, nid.value))
+            offs = np.empty(n.value + 1, dtype=np.int64)
+            check(lib.nnm_csv_fetch(h, values.ctypes.data, buf, offs.ctypes.data))
+            raw = buf.raw[: nid.value]
+            ids = [raw[offs[i]:offs[i + 1]].decode("utf-8") for i in range(n.value)]
+        else:
+            check(lib.nnm_csv_fetch(h, values.ctypes.data, None, None))
+    finally:
+        lib.nnm_csv_free(h)
+    return values, ids

@@ -35,6 +35,17 @@
 #include "nnm_kernels.cuh"
 #include "nnm_tc.cuh"
 
+// native CSV ingestion (nnm_csv.cpp)
+int nnm_csv_parse_impl(const char* path, char delim, const char* id_column, int threads,
+                       nnm_csv** out, std::string& err);
+int64_t nnm_csv_rows(const nnm_csv* c);
+int64_t nnm_csv_cols(const nnm_csv* c);
+bool nnm_csv_has_ids(const nnm_csv* c);
+void nnm_csv_copy_values(const nnm_csv* c, double* out);
+int64_t nnm_csv_id_bytes(const nnm_csv* c);
+void nnm_csv_copy_ids(const nnm_csv* c, char* buf, int64_t* offsets);
+void nnm_csv_destroy(nnm_csv* c);
+
 using namespace nnm;
 
 // ----------------------------------------------------------------------------
@@ -59,6 +70,7 @@ struct NnmError {
 [[noreturn]] void invalid(const std::string& m) { throw NnmError{NNM_E_INVALID, m}; }
 
 thread_local cudaStream_t t_alloc_stream = nullptr;  // stream for DevBuf allocations
+
 
 template <class F>
 int guarded(F&& f) {
@@ -151,15 +163,18 @@ __device__ __forceinline__ double bitsd(unsigned long long b) {
 }
 
 // X64 (row-major) -> X32 SoA [d][ld] rounded to nearest, +inf padding.
+// FP32 SoA copy + input checks on the device: chk[0] = first row holding a non-finite
+// value (model.py:29-76 message), chk[1] = 1 if a finite value is beyond the FP32 screen
 __global__ void prepare_kernel(const double* __restrict__ X64, int64_t n, int d, int64_t ld,
-                               float* __restrict__ X32, int* range_err) {
+                               float* __restrict__ X32, unsigned long long* chk) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= ld) return;
   for (int k = 0; k < d; ++k) {
     float v = INFINITY;
     if (i < n) {
       double x = X64[i * d + k];
-      if (!(fabs(x) <= 1e18)) atomicExch(range_err, 1);
+      if (!isfinite(x)) atomicMin(chk, (unsigned long long)i);
+      else if (!(fabs(x) <= 1e18)) atomicExch(chk + 1, 1ull);
       v = __double2float_rn(x);
     }
     X32[(int64_t)k * ld + i] = v;
@@ -2158,10 +2173,6 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
     invalid("dataset must have at least 1 point and 1 feature, got " + std::to_string(n) + "x" +
             std::to_string(d));
   if (n >= (int64_t)1 << 31) throw NnmError{NNM_E_UNSUPPORTED, "n must be < 2^31"};
-  if (!on_device) {
-    for (int64_t i = 0; i < n * d; ++i)
-      if (!std::isfinite(X[i])) invalid("non-finite feature value in row " + std::to_string(i / d + 1));
-  }
   int sms = 0;
   init_device(device, &sms);
   auto* ds = new nnm_dataset();
@@ -2183,13 +2194,18 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
     CUDA_TRY(cudaMemcpyAsync(ds->X64.p, X, (size_t)n * d * sizeof(double),
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ds->st));
     ds->X32.ensure((size_t)ds->ld * d);
-    ds->flag.ensure(1);
-    CUDA_TRY(cudaMemsetAsync(ds->flag.p, 0, sizeof(int), ds->st));
+    DevBuf<unsigned long long> chk;
+    chk.ensure(2);
+    const unsigned long long init[2] = {~0ull, 0ull};
+    CUDA_TRY(cudaMemcpyAsync(chk.p, init, sizeof(init), cudaMemcpyHostToDevice, ds->st));
     prepare_kernel<<<blocks_for(ds->ld), 256, 0, ds->st>>>(ds->X64.p, n, d, ds->ld, ds->X32.p,
-                                                          ds->flag.p); note_launch();
+                                                          chk.p); note_launch();
     CUDA_TRY(cudaGetLastError());
-    int range_err = ds->read1(ds->flag.p);
-    if (range_err)
+    unsigned long long h[2];
+    CUDA_TRY(cudaMemcpyAsync(h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, ds->st));
+    ds->sync();
+    if (h[0] != ~0ull) invalid("non-finite feature value in row " + std::to_string(h[0] + 1));
+    if (h[1])
       throw NnmError{NNM_E_UNSUPPORTED,
                      "feature magnitude above 1e18 is outside the FP32 screening range"};
   } catch (...) {
@@ -2230,6 +2246,33 @@ int nnm_dataset_create_device(const double* X_dev, int64_t n, int32_t d, int32_t
     if (!X_dev || !out) invalid("null argument");
     *out = make_dataset(X_dev, true, n, d, device);
   });
+}
+
+int nnm_csv_load(const char* path, char delimiter, const char* id_column, int32_t threads,
+                 nnm_csv** out, int64_t* n, int64_t* d, int32_t* has_ids, int64_t* id_bytes) {
+  return guarded([&] {
+    if (!path || !out) invalid("null argument");
+    std::string err;
+    nnm_csv* c = nullptr;
+    if (nnm_csv_parse_impl(path, delimiter, id_column, threads, &c, err) != 0) invalid(err);
+    *out = c;
+    if (n) *n = nnm_csv_rows(c);
+    if (d) *d = nnm_csv_cols(c);
+    if (has_ids) *has_ids = nnm_csv_has_ids(c) ? 1 : 0;
+    if (id_bytes) *id_bytes = nnm_csv_id_bytes(c);
+  });
+}
+
+int nnm_csv_fetch(nnm_csv* c, double* values, char* id_buf, int64_t* id_offsets) {
+  return guarded([&] {
+    if (!c) invalid("null table");
+    if (values) nnm_csv_copy_values(c, values);
+    if (id_buf && id_offsets && nnm_csv_has_ids(c)) nnm_csv_copy_ids(c, id_buf, id_offsets);
+  });
+}
+
+int nnm_csv_free(nnm_csv* c) {
+  return guarded([&] { nnm_csv_destroy(c); });
 }
 
 int nnm_dataset_destroy(nnm_dataset* ds) {

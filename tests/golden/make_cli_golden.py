@@ -40,9 +40,30 @@ PARSE_CASES = {
     "bad_id_name": "a,b\n1,2\n",
     "id_index_out_of_range": "1,2\n3,4\n",
     "spaces": " 1 , 2 \n 3 ,4\n",
+    "underscores": "1_000,2.5_5\n3e1_0,-_4\n",
+    "underscores_ok": "1_000,2.5_5\n3e1_0,4_4.0_1\n",
+    "bad_underscore": "1__0,2\n",
+    "inf_words": "INF,-Infinity\n",
+    "nan_word": "1,NaN\n",
+    "hex": "0x10,1\n",
+    "exp_forms": "1E5,.5\n5.,-1e-3\n+2,1e+02\n",
+    "crlf_cr": "1,2\r\n3,4\r5,6\r\n",
+    "vt_ff_seps": "1,2\x0b3,4\x0c5,6\x1c7,8\n",
+    "unicode_space": "\u00a01,2\u2003\n3,\u30004\n",
+    "tabs": "\t1\t,2\n3,4\t\n",
+    "quote_token": "1,2\n3,it's\n",
+    "id_index_str": "a,b,c\n1,2,3\n4,5,6\n",
+    "id_index_padded": "1,2,3\n4,5,6\n",
+    "id_index_neg": "1,2\n3,4\n",
+    "id_header_numeric_name": "x,1,y\n5,p,6\n7,q,8\n",
+    "header_mixed": "1,b,3\n4,5,6\n",
+    "trailing_delim": "1,2,\n3,4,\n",
+    "empty_field": "1,,3\n",
+    "semicolons_in_field": "1;2,3\n",
 }
 PARSE_ID = {"id_by_name": "id", "id_by_index": "1", "dup_id": "id", "bad_id_name": "zz",
-            "id_index_out_of_range": "5"}
+            "id_index_out_of_range": "5", "id_index_str": "2", "id_index_padded": " 01 ",
+            "id_index_neg": "-1", "id_header_numeric_name": "1"}
 
 
 def parse_cases(tmp):

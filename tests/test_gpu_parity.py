@@ -230,3 +230,19 @@ def test_boruvka_shuffled_blobs_vs_oracle(nnm):
         for f in FIELDS:
             assert np.array_equal(got[f], m_or[f]), (cons, f)
         assert np.array_equal(res.assignments, a_or)
+
+
+def test_device_input_checks(nnm):
+    """C-ABI input validation runs on the device (model.py:29-76 message, first bad row)."""
+    from paper_1402_3789_b200 import _native
+    from paper_1402_3789_b200.model import ValidationError
+
+    X = np.zeros((5000, 4))
+    X[3210, 2] = np.nan
+    X[4000, 1] = np.inf
+    with pytest.raises(ValidationError, match="non-finite feature value in row 3211"):
+        _native.DeviceDataset(X)
+    Y = np.ones((100, 3))
+    Y[7, 0] = 3e18
+    with pytest.raises(_native.NativeError, match="FP32 screening range"):
+        _native.DeviceDataset(Y)
