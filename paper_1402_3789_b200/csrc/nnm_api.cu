@@ -2194,6 +2194,7 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
     CUDA_TRY(cudaMemcpyAsync(ds->X64.p, X, (size_t)n * d * sizeof(double),
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ds->st));
     ds->X32.ensure((size_t)ds->ld * d);
+    ds->flag.ensure(1);  // scratch flag of the view build / pointer jumping
     DevBuf<unsigned long long> chk;
     chk.ensure(2);
     const unsigned long long init[2] = {~0ull, 0ull};
