@@ -91,6 +91,8 @@ typedef struct {
   double replay_ms;        /* edge sort + union-find replay into the merge log */
   int64_t tc_items;        /* ordered 128x128 tile pairs run through the tensor-core scan
                               (each a 128x128x32 kind::tf32 MMA); 0 on the FP32 path */
+  int64_t round_rescans;   /* round path: rounds whose reused row bounds were too loose, so
+                              the full scan ran (rounds - 1 - round_rescans were reused) */
 } nnm_stats;
 
 int nnm_abi_version(void);

@@ -52,7 +52,7 @@ class Stats(ctypes.Structure):
                 ("exact_evals", ctypes.c_int64), ("boruvka_rounds", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("pairs_covered", ctypes.c_double),
                 ("prep_ms", ctypes.c_double), ("replay_ms", ctypes.c_double),
-                ("tc_items", ctypes.c_int64)]
+                ("tc_items", ctypes.c_int64), ("round_rescans", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}

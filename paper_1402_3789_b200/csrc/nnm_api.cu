@@ -1059,12 +1059,17 @@ struct CandLess {
 template <int M>
 __global__ void rowpairs_kernel(const double* __restrict__ X64, int n, int d,
                                 const unsigned long long* __restrict__ B1, double thr, Cand* out,
-                                unsigned long long* count) {
+                                unsigned long long* count, const int* __restrict__ comp,
+                                const int* __restrict__ psize, int ksum) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   unsigned long long k = B1[i];
   if (!key_valid(k)) return;
   int j = (int)key_index(k);
+  // B1 may come from an earlier snapshot (round-path reuse): keep the pair only if it is
+  // still eligible (eligibility only shrinks as clusters merge and grow)
+  if (comp[i] == comp[j]) return;
+  if (ksum != INT_UNSET && psize[i] + psize[j] > ksum) return;
   if (!(i < j)) {
     unsigned long long kj = B1[j];
     if (key_valid(kj) && (int)key_index(kj) == i) return;  // emitted by row j
@@ -1298,6 +1303,8 @@ struct nnm_dataset {
   const int2* p1_list = nullptr;
   // round path
   DevBuf<Cand> cands, cands2;
+  DevBuf<unsigned long long> rB1;  // round path: per-row best screened key (may be stale)
+  bool rb1_valid = false;
   DevBuf<int> active, rmap, rsize;
   DevBuf<int2> kv;
   nnm_stats stats{};
@@ -2058,25 +2065,30 @@ struct nnm_dataset {
   // ---------------------------------------------------------------- top-P
   // Exact top-P eligible pairs for the current (comp, psize) snapshot.
   template <int M>
-  void rowpairs_t(double thr, unsigned long long* cnt) {
-    rowpairs_kernel<M><<<blocks_for(n), 256, 0, st>>>(X64.p, (int)n, d, B1.p, thr, cands.p, cnt); note_launch();
+  void rowpairs_t(const unsigned long long* b1, double thr, unsigned long long* cnt,
+                  const int* psz, int ksum) {
+    rowpairs_kernel<M><<<blocks_for(n), 256, 0, st>>>(X64.p, (int)n, d, b1, thr, cands.p, cnt,
+                                                     comp.p, psz, ksum); note_launch();
   }
 
-  void top_p(int metric, double thr, int kl2, int kl3, int64_t P, std::vector<Cand>& out) {
-    ensure_norms(metric);
-    use_original_view();
-    dot_on = false;
-    em = make_err_model(metric, d);
-    float thr_hi = std::isinf(thr) ? INFINITY : float_up(screen_upper(em, thr, 2.0 * maxnorm));
-    B1.ensure(n);
-    scan(metric, B1.p, nullptr, false, kl2, kl3, thr_hi, 0, tile_pairs());
+  // Exact top-P eligible pairs for the current (comp, psize) snapshot.
+  //   * rB1: per-row best screened key over eligible partners (full FP32 scan);
+  //   * tau: P-th smallest exact row-best pair (an upper bound of the P-th key);
+  //   * every top-P pair has both endpoints in A = {i : exact_lower(rB1_i) <= tau};
+  //     the A x A pairs under the screened bound are evaluated exactly, sorted, cut at P.
+  // reuse (rounds of one run): eligibility only shrinks as clusters merge, so the rB1 of
+  // an earlier snapshot still bounds every eligible partner from below and its row-best
+  // pairs that are still eligible are real candidates: the full scan is skipped until
+  // A grows past n/8 (or fewer than P row-best pairs survive) -- SURVEY 8(f) rank 2.
+  bool top_p_pass(int metric, double thr, int kl2, int kl3, int64_t P, const int* psz, int ksum,
+                  int64_t max_active, std::vector<Cand>& out) {
     counters.ensure(8);
     cands.ensure(n);
     CUDA_TRY(cudaMemsetAsync(counters.p + 3, 0, 3 * sizeof(unsigned long long), st));
     switch (metric) {
-      case MANHATTAN: rowpairs_t<MANHATTAN>(thr, counters.p + 3); break;
-      case CHEBYSHEV: rowpairs_t<CHEBYSHEV>(thr, counters.p + 3); break;
-      default: rowpairs_t<EUCLIDEAN>(thr, counters.p + 3);
+      case MANHATTAN: rowpairs_t<MANHATTAN>(rB1.p, thr, counters.p + 3, psz, ksum); break;
+      case CHEBYSHEV: rowpairs_t<CHEBYSHEV>(rB1.p, thr, counters.p + 3, psz, ksum); break;
+      default: rowpairs_t<EUCLIDEAN>(rB1.p, thr, counters.p + 3, psz, ksum);
     }
     CUDA_TRY(cudaGetLastError());
     int64_t nc = (int64_t)read1(counters.p + 3);
@@ -2086,12 +2098,43 @@ struct nnm_dataset {
       thrust::sort(thrust::cuda::par(talloc).on(st), cands.p, cands.p + nc, CandLess());
       Cand c = read1(cands.p + (P - 1));
       tau = c.d;
+    } else if (max_active < n) {
+      return false;  // too few surviving row-best pairs: rescan
     }
     active.ensure(n);
-    active_rows_kernel<<<blocks_for(n), 256, 0, st>>>((int)n, B1.p, norm.p, maxnorm, em, tau,
+    active_rows_kernel<<<blocks_for(n), 256, 0, st>>>((int)n, rB1.p, norm.p, maxnorm, em, tau,
                                                       active.p, counters.p + 4); note_launch();
     CUDA_TRY(cudaGetLastError());
     int64_t na = (int64_t)read1(counters.p + 4);
+    if (na > max_active) return false;
+    top_p_collect(metric, thr, kl2, kl3, P, tau, na, out);
+    return true;
+  }
+
+  void top_p(int metric, double thr, int kl2, int kl3, int64_t P, std::vector<Cand>& out,
+             bool reuse = false) {
+    ensure_norms(metric);
+    use_original_view();
+    dot_on = false;
+    em = make_err_model(metric, d);
+    float thr_hi = std::isinf(thr) ? INFINITY : float_up(screen_upper(em, thr, 2.0 * maxnorm));
+    rB1.ensure(n);
+    const int ksum = size_rule(kl2, kl3);
+    const char* re = getenv("NNM_ROUND_REUSE");
+    if (reuse && rb1_valid && !(re && re[0] == '0')) {
+      const int* psz = ksum != INT_UNSET ? eff_sizes(kl2) : comp.p;
+      if (top_p_pass(metric, thr, kl2, kl3, P, psz, ksum, std::max<int64_t>(2 * P, n / 8), out))
+        return;
+      ++stats.round_rescans;
+    }
+    scan(metric, rB1.p, nullptr, false, kl2, kl3, thr_hi, 0, tile_pairs());
+    rb1_valid = true;
+    const int* psz = ksum != INT_UNSET ? eff_sizes(kl2) : comp.p;
+    top_p_pass(metric, thr, kl2, kl3, P, psz, ksum, n, out);
+  }
+
+  void top_p_collect(int metric, double thr, int kl2, int kl3, int64_t P, double tau, int64_t na,
+                     std::vector<Cand>& out) {
     out.clear();
     if (na < 2) return;
     // deterministic order of the active set (atomics appended in arbitrary order)
@@ -2388,6 +2431,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
     } else {
       // ---------------- top-P rounds with exact engine semantics
       ds->stats.path = NNM_PATH_ROUNDS;
+      ds->rb1_valid = false;
       const int64_t kl1 = cons->kl1, kl2 = cons->kl2, kl3 = cons->kl3, kl4 = cons->kl4;
       double thr = INFINITY;
       if (!std::isnan(cons->dmax)) thr = metric == EUCLIDEAN ? cons->dmax * cons->dmax : cons->dmax;
@@ -2420,7 +2464,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       for (;;) {
         if (count == 1) { reason = NNM_STOP_SINGLE_CLUSTER; break; }
         if (kl1 > 0 && count <= kl1) { reason = NNM_STOP_KL1; break; }
-        ds->top_p(metric, thr, clamp_int(kl2, ds->n), clamp_int(kl3, ds->n), P, buf);
+        ds->top_p(metric, thr, clamp_int(kl2, ds->n), clamp_int(kl3, ds->n), P, buf, rounds > 0);
         if (buf.empty()) { reason = NNM_STOP_NO_ELIGIBLE; break; }
         ++rounds;
         const int64_t L = (int64_t)buf.size();

@@ -246,3 +246,31 @@ def test_device_input_checks(nnm):
     Y[7, 0] = 3e18
     with pytest.raises(_native.NativeError, match="FP32 screening range"):
         _native.DeviceDataset(Y)
+
+
+def test_round_path_reuse_equals_full_rescans():
+    """Round path (kl1..kl4, P=256): reusing earlier row bounds (default) gives the same
+    merges, rounds and counters as a full scan every round (NNM_ROUND_REUSE=0)."""
+    import os
+    import subprocess
+    import sys
+
+    from nnm_testutil import ROOT
+
+    code = ("import hashlib, numpy as np, paper_1402_3789_b200 as nnm\n"
+            "a = nnm.generate_synthetic(16000, 25, 32, 1.0, seed=2)[0]\n"
+            "b = nnm.generate_synthetic(4000, 25, 80, 3.0, seed=3)[0]\n"
+            "X = np.vstack([a, b])\n"
+            "r = nnm.fit(X, kl1=80, kl2=300, kl3=450, kl4=150, pairs_per_batch=256)\n"
+            "c = np.array([[v for v in d.values()] for d in r.round_counters])\n"
+            "print(hashlib.sha256(r.merges.array.tobytes() + r.assignments.tobytes() + c.tobytes())"
+            ".hexdigest(), r.rounds, r.device_stats['round_rescans'])\n")
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, NNM_ROUND_REUSE=flag)
+        p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(p.stdout.split())
+    assert outs[0][0] == outs[1][0] and outs[0][1] == outs[1][1]
+    assert int(outs[0][1]) > 20  # a multi-round run that exercised the reuse
