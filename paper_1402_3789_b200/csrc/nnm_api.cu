@@ -2016,6 +2016,7 @@ struct nnm_dataset {
       CUDA_TRY(cudaMemcpyAsync(h, replay.p, ne * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st));
       sync();
     }
+    auto tq0 = std::chrono::steady_clock::now();
     // union-find replay (model.py:109-187): union keeps the smaller root (int32 forest,
     // path halving; roots are always the minimum index of their cluster)
     std::vector<int32_t> par(n), sz(n, 1);
@@ -2035,7 +2036,12 @@ struct nnm_dataset {
     };
     int reason = stop_of(count);
     if (!reason) {
+      constexpr unsigned long long kAhead = 16;  // prefetch the forest entries of later merges
       for (unsigned long long t = 0; t < ne; ++t) {
+        if (t + kAhead < ne) {
+          __builtin_prefetch(&par[h[t + kAhead].a], 1);
+          __builtin_prefetch(&par[h[t + kAhead].b], 1);
+        }
         const ReplayEdge& e = h[t];
         const int32_t ra = find(e.a), rb = find(e.b);
         if (ra == rb) throw NnmError{NNM_E_CUDA, "boruvka produced a cycle (internal error)"};
@@ -2056,10 +2062,15 @@ struct nnm_dataset {
       }
       if (!reason) reason = NNM_STOP_NO_ELIGIBLE;
     }
+    auto tq1 = std::chrono::steady_clock::now();
     for (int64_t i = 0; i < n; ++i) assign[i] = find((int32_t)i);
     *n_merges = nm;
     *rounds = (n > 1 && stop_of(n) == 0) ? bv_round : 0;
     *stop = reason;
+    if (getenv("NNM_DEBUG"))
+      fprintf(stderr, "[nnm] replay: loop %.1f ms, assign %.1f ms\n",
+              std::chrono::duration<double, std::milli>(tq1 - tq0).count(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq1).count());
   }
 
   // ---------------------------------------------------------------- top-P
