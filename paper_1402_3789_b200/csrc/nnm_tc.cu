@@ -48,8 +48,8 @@ namespace {
 constexpr int TC_STAGES = 8;
 constexpr int TC_EPI_WARPS = 8;                        // warps 0-7: 2 groups x 4 lane quadrants
 constexpr int TC_EPI_GROUPS = 2;                       // epilogue groups, alternating items
-constexpr int TC_PREP_GROUPS = 2;                      // 2 x 2 prep warps, alternating items
-constexpr int TC_PREP_THREADS = 64;                    // per group; each thread owns 2 columns
+constexpr int TC_PREP_GROUPS = 4;                      // 4 single-warp prep groups, items q % 4
+constexpr int TC_PREP_THREADS = 32;                    // per group; each lane owns 4 rows / columns
 constexpr int TC_PRODUCER_WARP = TC_EPI_WARPS + TC_PREP_GROUPS * TC_PREP_THREADS / 32;
 constexpr int TC_MMA_WARP = TC_PRODUCER_WARP + 1;
 constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;     // 448: <= 4 warps per SMSP -> 128 regs
@@ -76,8 +76,9 @@ struct TcSmem {
   float erow[TC_STAGES][TILE];
   float etarow[TC_STAGES][TILE];
   int2 ring[TC_RING];                  // (I, J) of item q at q % TC_RING (written by the producer)
+  int ringrt[TC_RING];                 // row-tile index of item q, negated-minus-one when item q
+                                       // is the first of its row tile (producer)
   int slot[2][8];
-  int slotcnt[TC_PREP_GROUPS][4];  // first-occurrence counts per 32-row block
   unsigned long long full[TC_STAGES], prepped[TC_STAGES], empty[TC_STAGES];
   unsigned long long tfull[TC_ACC], tempty[TC_ACC], afull[2], aprepped[2], aempty[2];
   uint32_t tmem_base;
@@ -101,19 +102,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
       "DONE:\n"
       "}\n" ::"r"(su32(b)),
       "r"(parity), "r"(0x989680u)  // suspend-time hint: a waiting warp sleeps, it does not poll
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait_spin(unsigned long long* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(su32(b)),
-      "r"(parity)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
@@ -143,10 +131,6 @@ __device__ __forceinline__ void tc_before() {
 __device__ __forceinline__ void tc_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void group_bar(int g) {  // the 64 threads of prep group g
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");
-}
-
 // K-major, 128-byte swizzled operand: rows of 128 B, 8-row atoms 1024 B apart (SBO),
 // descriptor version 1 (sm_100), layout type 2 (SWIZZLE_128B).
 __device__ __forceinline__ uint64_t sw128_desc(const void* p) {
@@ -176,16 +160,6 @@ __device__ __forceinline__ void mma_commit(unsigned long long* bar) {
 
 #define TC_R8(i) "=r"(r[i]), "=r"(r[i + 1]), "=r"(r[i + 2]), "=r"(r[i + 3]), \
                  "=r"(r[i + 4]), "=r"(r[i + 5]), "=r"(r[i + 6]), "=r"(r[i + 7])
-__device__ __forceinline__ void tmem_ld32x(uint32_t taddr, float (&v)[32]) {
-  uint32_t* r = reinterpret_cast<uint32_t*>(v);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : TC_R8(0), TC_R8(8), TC_R8(16), TC_R8(24)
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&v)[64]) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
   asm volatile(
@@ -215,13 +189,6 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
                : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
-  uint32_t r;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-  return __uint_as_float(r);
-}
-
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -345,44 +312,34 @@ __device__ __forceinline__ void load_row(const float* tile, int r, int d, float 
   }
 }
 
-__device__ __forceinline__ float max32(const float* v) {
-  float t[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) t[k] = fmaxf(v[2 * k], v[2 * k + 1]);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) t[k] = fmaxf(t[2 * k], t[2 * k + 1]);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) t[k] = fmaxf(t[2 * k], t[2 * k + 1]);
-  return fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3]));
-}
-
 // Mask slots of a row tile: the first kc distinct components in position order
-// (parallel first-occurrence test + warp ballots).  Called by one prep group: thread
-// pt (0..63) owns rows pt and pt + 64.
-__device__ __forceinline__ void select_slots(const int* comp, int* slot, int* cnt, int g, int pt,
-                                             int kc) {
-  const int ca = comp[pt], cb = comp[pt + 64];
-  bool fa = ca >= 0, fb = cb >= 0;
+// (parallel first-occurrence test + warp ballots).  Called by one prep warp: lane l owns
+// rows l, l + 32, l + 64, l + 96 (one 32-row block per ballot, in position order).
+__device__ __forceinline__ void select_slots(const int* comp, int* slot, int lane, int kc) {
+  int c[4];
+  bool f[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    c[b] = comp[lane + 32 * b];
+    f[b] = c[b] >= 0;
+  }
 #pragma unroll 8
   for (int r = 0; r < TILE; ++r) {
-    const int c = comp[r];
-    fa &= !(r < pt && c == ca);
-    fb &= !(r < pt + 64 && c == cb);
+    const int cr = comp[r];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) f[b] &= !(r < lane + 32 * b && cr == c[b]);
   }
-  const unsigned ma = __ballot_sync(0xFFFFFFFFu, fa), mb = __ballot_sync(0xFFFFFFFFu, fb);
-  const int w = pt >> 5, lane = pt & 31;  // 32-row blocks in position order: a0 a1 b0 b1
-  if (lane == 0) {
-    cnt[w] = __popc(ma);
-    cnt[2 + w] = __popc(mb);
-  }
-  group_bar(g);
+  int base = 0;
   const unsigned below = (1u << lane) - 1u;
-  const int ra = __popc(ma & below) + (w ? cnt[0] : 0);
-  const int rb = __popc(mb & below) + cnt[0] + cnt[1] + (w ? cnt[2] : 0);
-  const int total = cnt[0] + cnt[1] + cnt[2] + cnt[3];
-  if (fa && ra < kc) slot[ra] = ca;
-  if (fb && rb < kc) slot[rb] = cb;
-  if (pt < 8 && pt >= min(total, kc)) slot[pt] = -2;
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, f[b]);
+    const int rank = base + __popc(m & below);
+    if (f[b] && rank < kc) slot[rank] = c[b];
+    base += __popc(m);
+  }
+  if (lane < 8 && lane >= min(base, kc)) slot[lane] = -2;
+  __syncwarp();
 }
 
 template <int DC>
@@ -451,6 +408,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         if (q >= TC_STAGES) mbar_wait(&S.empty[s], ((q / TC_STAGES) - 1) & 1);
         trace(p, 0, q, 0);
         S.ring[q % TC_RING] = it;  // published to the other roles by the full barrier
+        S.ringrt[q % TC_RING] = (q == 0 || it.x != S.ring[(q - 1) % TC_RING].x) ? -rt - 1 : rt;
         mbar_expect_tx(&S.full[s], TC_TILE_BYTES + TC_META * 4 + 2 * TILE * 4);
         bulk_g2s(S.B[s], p.img + (int64_t)it.y * TC_TILE_FLOATS, TC_TILE_BYTES, &S.full[s]);
         bulk_g2s(S.metaB[s], p.meta + (int64_t)it.y * TC_META, TC_META * 4, &S.full[s]);
@@ -477,7 +435,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         trace(p, 1, q, 0);
         tc_after();
         const uint64_t ad = sw128_desc(S.A[rt & 1]), bd = sw128_desc(S.B[s]);
-        const int reps = (p.dbg & 32) ? 8 : 1;  // timing experiment: repeat the MMAs
+        const int reps = (p.dbg & 512) ? 0 : (p.dbg & 32) ? 8 : 1;  // timing experiments
         for (int rep = 0; rep < reps; ++rep) {
 #pragma unroll
           for (int kk = 0; kk < TC_K / 8; ++kk)  // K = 8 tf32 (32 B) per instruction
@@ -489,62 +447,55 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
     }
   } else if (warp >= TC_EPI_WARPS) {
     // ------------------------------------------------------------ prep groups
-    // group g preps items q = g, g + 2, ...; thread pt owns columns / rows pt and pt + 64.
-    // Row-tile changes are read from the item ring (entries q-2 .. q are still live: the
-    // producer runs at most TC_STAGES items ahead of the slowest consumer, TC_RING >> that)
-    const int g = (warp - TC_EPI_WARPS) / (TC_PREP_THREADS / 32);
-    const int pt = tid - TC_EPI_WARPS * 32 - g * TC_PREP_THREADS;
+    // group g (one warp) preps items q = g, g + 4, ...; lane l owns rows / columns
+    // l + 32k (k < 4).  Row-tile changes are read from the item ring (entries q-4 .. q
+    // are still live: the producer runs at most TC_STAGES items ahead of the slowest
+    // consumer and TC_RING >> TC_STAGES + 4)
+    const int g = warp - TC_EPI_WARPS;
+    const int pt = lane;
     int rt = -1, myI = -1;
-    float xa[32], xb2[32];
-    float tna = 0.f, tnb = 0.f, eta_a = 0.f, eta_b = 0.f;
+    float tn4[4] = {0.f, 0.f, 0.f, 0.f}, eta4[4] = {0.f, 0.f, 0.f, 0.f};
     int slot[8];
     for (int q = g; q < nq; q += TC_PREP_GROUPS) {
       const int s = q % TC_STAGES;
       mbar_wait(&S.full[s], (q / TC_STAGES) & 1);
       if (pt == 0) trace(p, 2, q, 0);
-      // row-tile index of item q (counted over all items, both groups)
+      // row-tile index of item q and whether it opens its row tile (from the producer)
       const int I = S.ring[q % TC_RING].x;
-      const int Im1 = q >= 1 ? S.ring[(q - 1) % TC_RING].x : -1;
-      if (rt < 0) {
-        rt = 0;
-        for (int k = 1; k <= q; ++k) rt += S.ring[k % TC_RING].x != S.ring[(k - 1) % TC_RING].x;
-      } else {
-        const int Im2 = S.ring[(q - 2) % TC_RING].x;
-        rt += (Im1 != Im2) + (I != Im1);
-      }
+      const int rtq = S.ringrt[q % TC_RING];
+      const bool opens = rtq < 0;
+      rt = opens ? -rtq - 1 : rtq;
       const int xb = rt & 1;
       if (I != myI) {
         myI = I;
-        tna = __ldg(p.tnorm + (int64_t)I * TILE + pt);
-        tnb = __ldg(p.tnorm + (int64_t)I * TILE + pt + 64);
-        eta_a = __ldg(p.eta + (int64_t)I * TILE + pt);
-        eta_b = __ldg(p.eta + (int64_t)I * TILE + pt + 64);
-        if (I != Im1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          tn4[k] = __ldg(p.tnorm + (int64_t)I * TILE + pt + 32 * k);
+          eta4[k] = __ldg(p.eta + (int64_t)I * TILE + pt + 32 * k);
+        }
+        if (opens) {
           // first item of the row tile: this group prepares the A operand
           mbar_wait(&S.afull[xb], (rt >> 1) & 1);
-          select_slots(S.acomp[xb], S.slot[xb], S.slotcnt[g], g, pt, kc);
-          group_bar(g);
+          select_slots(S.acomp[xb], S.slot[xb], pt, kc);
 #pragma unroll
           for (int k = 0; k < 8; ++k) slot[k] = S.slot[xb][k];
-          load_row(S.A[xb], pt, d, xa);
-          load_row(S.A[xb], pt + 64, d, xb2);
-          write_tail(S.A[xb], pt, d, kc, 1.f, 1.f, slot_hits(S.acomp[xb][pt], slot), TC_MASK);
-          write_tail(S.A[xb], pt + 64, d, kc, 1.f, 1.f, slot_hits(S.acomp[xb][pt + 64], slot),
-                     TC_MASK);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int row = pt + 32 * k;
+            write_tail(S.A[xb], row, d, kc, 1.f, 1.f, slot_hits(S.acomp[xb][row], slot), TC_MASK);
+          }
           fence_proxy_async();
-          group_bar(g);
+          __syncwarp();
           if (pt == 0) mbar_arrive(&S.aprepped[xb]);
         } else {
-          // the other group prepared it: wait, then take the slots and the rows
+          // another group prepared it: wait, then take the slots
           mbar_wait(&S.aprepped[xb], (rt >> 1) & 1);
 #pragma unroll
           for (int k = 0; k < 8; ++k) slot[k] = S.slot[xb][k];
-          load_row(S.A[xb], pt, d, xa);
-          load_row(S.A[xb], pt + 64, d, xb2);
         }
       }
       if (p.dbg & 2) {  // timing experiment: no prep work
-        group_bar(g);
+        __syncwarp();
         if (pt == 0) mbar_arrive(&S.prepped[s]);
         continue;
       }
@@ -554,16 +505,19 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
       const float dnorm = tc_dnorm(dn2, d);
       const float RJ = S.metaB[s][32], etaJ = S.metaB[s][33];
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        // row pt + 64 half: r_i and its bounds for the epilogue
-        const int row = pt + 64 * half;
-        const float r = tc_r(S.asq[xb][row], tc_dot(half ? xb2 : xa, dl, d), dn2);
+      for (int k = 0; k < 4; ++k) {
+        // row pt + 32k: r_i and its bounds for the epilogue (coordinates read from the
+        // A tile: the tail chunk holds the A-side constants, not coordinates < d)
+        const int row = pt + 32 * k;
+        float x[32];
+        load_row(S.A[xb], row, d, x);
+        const float r = tc_r(S.asq[xb][row], tc_dot(x, dl, d), dn2);
         float Erow, eta_row;
-        tc_bounds(dnorm, d, half ? tnb : tna, half ? eta_b : eta_a, RJ, etaJ, Erow, eta_row);
+        tc_bounds(dnorm, d, tn4[k], eta4[k], RJ, etaJ, Erow, eta_row);
         S.rrow[s][row] = r;
         S.erow[s][row] = Erow;
         S.etarow[s][row] = eta_row;
-        // column pt + 64 half: s_j = |y|^2 + 2 D.y into the K tail (hi / lo), slot hits
+        // column pt + 32k: s_j = |y|^2 + 2 D.y into the K tail (hi / lo), slot hits
         const int col = row;
         float y[32];
         load_row(S.B[s], col, d, y);
@@ -583,7 +537,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
       if (pt == 0) trace(p, 5, q, 1);
       if (!(p.dbg & 4)) fence_proxy_async();  // (dbg 4: timing experiment only)
       if (pt == 0) trace(p, 7, q, 0);
-      group_bar(g);
+      __syncwarp();
       if (pt == 0) {
         trace(p, 2, q, 1);
         mbar_arrive(&S.prepped[s]);
