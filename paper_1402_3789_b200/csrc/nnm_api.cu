@@ -614,39 +614,57 @@ __device__ __forceinline__ double tile_lb32(float dc, float cnI, float cnJ, floa
   return (M == EUCLIDEAN || M == SQEUCLIDEAN) ? r * r * (1.0 - 1e-9) : r * (1.0 - 1e-9);
 }
 
-// Full-square item list for the tensor-core scan: out[2w] = (I, J), out[2w+1] = (J, I);
-// the diagonal twin and (with umax) every orientation whose rigorous tile lower bound
-// exceeds the row tile's component bound become the sentinel (INT_MAX, INT_MAX).
+// Full-square item list for the tensor-core scan.  Item (I, J) serves the rows of tile I;
+// it is keyed (I << 32 | fp32 bits of the centre distance) so that, after one radix sort,
+// each row tile visits its nearest column tiles first (the diagonal tile, distance 0,
+// leads) and its rows' thresholds tighten early.  With umax (phase 2) an orientation
+// whose rigorous tile lower bound exceeds the row tile's component bound is dropped; the
+// dropped ones and the diagonal twin become the sentinel key ~0 (sorted last, counted).
 __global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n,
                                  const double* __restrict__ umax, const float* __restrict__ c32,
                                  const float* __restrict__ cn, const float* __restrict__ r32, int T,
-                                 int d, int metric, int2* __restrict__ out,
-                                 unsigned long long* __restrict__ dropped) {
+                                 int d, int metric, unsigned long long* __restrict__ keys,
+                                 int* __restrict__ js, unsigned long long* __restrict__ dropped) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned drop = 0;
   if (w < n) {
     const int2 it = items[w];
-    const int2 none = make_int2(0x7FFFFFFF, 0x7FFFFFFF);
     bool keep_ij = true, keep_ji = it.x != it.y;
-    if (umax && it.x != it.y) {
+    float dc = 0.f;
+    if (it.x != it.y) {
       // same fp32 centre distance and bound as enum_count_kernel (the item passed it)
       const float* ci = c32 + it.x;  // strided view: ci[k * T] is coordinate k of tile I
       double lb;
-      if (metric == MANHATTAN)
-        lb = tile_lb32<MANHATTAN>(cdist32s<MANHATTAN>(c32, T, ci, it.y, d), cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
-      else if (metric == CHEBYSHEV)
-        lb = tile_lb32<CHEBYSHEV>(cdist32s<CHEBYSHEV>(c32, T, ci, it.y, d), cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
-      else
-        lb = tile_lb32<EUCLIDEAN>(cdist32s<EUCLIDEAN>(c32, T, ci, it.y, d), cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
-      keep_ij = lb <= umax[it.x];
-      keep_ji = lb <= umax[it.y];
+      if (metric == MANHATTAN) {
+        dc = cdist32s<MANHATTAN>(c32, T, ci, it.y, d);
+        lb = tile_lb32<MANHATTAN>(dc, cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
+      } else if (metric == CHEBYSHEV) {
+        dc = cdist32s<CHEBYSHEV>(c32, T, ci, it.y, d);
+        lb = tile_lb32<CHEBYSHEV>(dc, cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
+      } else {
+        dc = cdist32s<EUCLIDEAN>(c32, T, ci, it.y, d);
+        lb = tile_lb32<EUCLIDEAN>(dc, cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
+      }
+      if (umax) {
+        keep_ij = lb <= umax[it.x];
+        keep_ji = lb <= umax[it.y];
+      }
     }
-    out[2 * w] = keep_ij ? it : none;
-    out[2 * w + 1] = keep_ji ? make_int2(it.y, it.x) : none;
+    const unsigned long long db = (unsigned long long)__float_as_uint(dc);
+    keys[2 * w] = keep_ij ? ((unsigned long long)it.x << 32 | db) : ~0ull;
+    js[2 * w] = it.y;
+    keys[2 * w + 1] = keep_ji ? ((unsigned long long)it.y << 32 | db) : ~0ull;
+    js[2 * w + 1] = it.x;
     drop = (keep_ij ? 0u : 1u) + (keep_ji ? 0u : 1u);
   }
   drop = __reduce_add_sync(0xFFFFFFFFu, drop);
   if ((threadIdx.x & 31) == 0 && drop) atomicAdd(dropped, (unsigned long long)drop);
+}
+
+__global__ void tc_items_kernel(const unsigned long long* __restrict__ keys, const int* __restrict__ js,
+                                int64_t n, int2* __restrict__ items) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < n) items[w] = make_int2((int)(keys[w] >> 32), js[w]);
 }
 
 // Phase 1: for each tile I the PK tile pairs with the smallest LB among tiles
@@ -1285,6 +1303,8 @@ struct nnm_dataset {
   bool tc_ready = false;
   DevBuf<float> tc_img, tc_tnorm, tc_eta, tc_meta, tc_sq;
   DevBuf<int2> tc_items;
+  DevBuf<unsigned long long> tc_keys;  // (I << 32 | centre-distance bits), radix-sorted
+  DevBuf<int> tc_js;
   // dot form
   bool dot_on = false;
   DotModel dm{};
@@ -1486,14 +1506,17 @@ struct nnm_dataset {
     counters.ensure(8);
     CUDA_TRY(cudaMemsetAsync(counters.p + 5, 0, sizeof(unsigned long long), st));
     // every dropped orientation / diagonal twin leaves a sentinel (sorted last), counted
+    tc_keys.ensure((size_t)2 * n_up);
+    tc_js.ensure((size_t)2 * n_up);
     tc_mirror_kernel<<<blocks_for(n_up), 256, 0, st>>>(items + w_begin, n_up, umax, tc32.p, tcn32.p,
-                                                       tr32.p, Tp, d, bv_metric, tc_items.p,
+                                                       tr32.p, Tp, d, bv_metric, tc_keys.p, tc_js.p,
                                                        counters.p + 5); note_launch();
     CUDA_TRY(cudaGetLastError());
-    auto* k64 = reinterpret_cast<unsigned long long*>(tc_items.p);
-    thrust::sort(thrust::cuda::par(talloc).on(st), k64, k64 + 2 * n_up, ItemLess());
+    thrust::sort_by_key(thrust::cuda::par(talloc).on(st), tc_keys.p, tc_keys.p + 2 * n_up, tc_js.p);
     const int64_t nfull = 2 * n_up - (int64_t)read1(counters.p + 5);
     if (nfull <= 0) return;
+    tc_items_kernel<<<blocks_for(nfull), 256, 0, st>>>(tc_keys.p, tc_js.p, nfull, tc_items.p); note_launch();
+    CUDA_TRY(cudaGetLastError());
     TcArgs a;
     a.img = tc_img.p;
     a.tnorm = tc_tnorm.p;
@@ -1519,8 +1542,8 @@ struct nnm_dataset {
     DevBuf<long long> trbuf;
     a.trace = nullptr;
     if (trf && nfull / grid >= 256) {
-      trbuf.ensure(8 * 256 * 2);
-      CUDA_TRY(cudaMemsetAsync(trbuf.p, 0, 8 * 256 * 2 * sizeof(long long), st));
+      trbuf.ensure(8 * 256 * 2 + 4);
+      CUDA_TRY(cudaMemsetAsync(trbuf.p, 0, (8 * 256 * 2 + 4) * sizeof(long long), st));
       a.trace = trbuf.p;
     }
     CUDA_TRY(cudaEventRecord(ev0, st));
@@ -1534,11 +1557,12 @@ struct nnm_dataset {
     stats.scans += 1;
     stats.tc_items += nfull;
     if (a.trace) {  // append the timeline of this launch (CTA 0, first 256 items)
-      std::vector<long long> h(8 * 256 * 2);
+      std::vector<long long> h(8 * 256 * 2 + 4);
       CUDA_TRY(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
       sync();
       if (FILE* f = fopen(trf, "a")) {
-        fprintf(f, "launch items %lld grid %d\n", (long long)nfull, grid);
+        fprintf(f, "launch items %lld grid %d exact_evals %lld seeds %lld slow_groups %lld\n", (long long)nfull,
+                grid, h[8 * 256 * 2], h[8 * 256 * 2 + 1], h[8 * 256 * 2 + 2]);
         const long long t0 = h[0];
         for (int q = 0; q < 256; ++q)
           fprintf(f, "%d prod %lld mma %lld prep %lld %lld epi_prepped %lld epi %lld %lld | ld %lld sums %lld tail %lld dn %lld fence %lld\n", q,

@@ -553,7 +553,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
     const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     int prevI = -1;
     unsigned long long k1 = NONE_KEY, k2 = NONE_KEY;
-    float gT = INFINITY;
+    float gT = INFINITY, tup = INFINITY;  // tup: seeded upper bound of the second best
     int ci = -1;
     int64_t g = 0;
     for (int q = e; q < nq; q += TC_EPI_GROUPS) {
@@ -571,6 +571,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         const unsigned long long gb = *((volatile const unsigned long long*)(p.B2 + g));
         gT = key_valid(gb) ? key_value(gb) : INFINITY;
         k1 = k2 = NONE_KEY;
+        tup = INFINITY;
       }
       const float r = S.rrow[s][i], Erow = S.erow[s][i], eta_row = S.etarow[s][i];
       // G' threshold equivalent to "L <= T may hold" (vthr: largest v with L <= T)
@@ -580,7 +581,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         const float vthr = (st * st + Erow) * 1.00001f;
         return (r - vthr) * 0.5f - (fabsf(r) + vthr) * 1e-6f - 1e-30f;
       };
-      float T = fminf(fminf(k2 == NONE_KEY ? INFINITY : key_value(k2), gT), p.thr_hi);
+      float T = fminf(fminf(k2 == NONE_KEY ? INFINITY : key_value(k2), fminf(gT, tup)), p.thr_hi);
       float gam = gamma_of(T);
       const int a = q % TC_ACC;
       mbar_wait(&S.tfull[a], (q / TC_ACC) & 1);
@@ -610,6 +611,35 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
             gm |= (ci >= 0 ? m : 0u) << (8 * hb);
           }
         }
+        // threshold seed: a row with no finite threshold yet (first items of a row tile in
+        // phase 1) would send every column to the FP64 path.  The two largest valid G' of the
+        // item give two distinct eligible partners with S <= (sqrt(v + E) + eta)^2, so the
+        // larger of those upper bounds caps the row's second-best exact value.
+        if (__any_sync(0xFFFFFFFFu, ci >= 0 && !(T < INFINITY))) {
+          float b1 = -INFINITY, b2 = -INFINITY;
+#pragma unroll 1
+          for (int gidx = 0; gidx < TILE / 8; ++gidx) {
+            float w[8];
+            tmem_ld8(lane_base + a * TILE + gidx * 8, w);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int cj = S.bcomp[s][gidx * 8 + u];
+              if (cj >= 0 && cj != ci) {
+                b2 = fmaxf(b2, fminf(b1, w[u]));
+                b1 = fmaxf(b1, w[u]);
+              }
+            }
+          }
+          if (p.trace && lane == 0) atomicAdd((unsigned long long*)(p.trace + 8 * 256 * 2 + 1), 1ull);
+          if (ci >= 0 && !(T < INFINITY) && b2 > -INFINITY) {
+            const double v2 = (double)__fmaf_rn(-2.f, b2, r);
+            const double e = (double)Erow * (1.0 + 1e-9) + 1.02 * 5.9604644775390625e-08 * fabs(v2);
+            const double up = sqrt(fmax(0.0, v2 + e)) * (1.0 + 1e-15) + (double)eta_row;
+            tup = float_up(up * up * (1.0 + 1e-15));
+            T = fminf(T, tup);
+            gam = gamma_of(T);
+          }
+        }
         // exact insert path (rare): the warp re-reads only the 8-column groups where some
         // lane may hold a candidate (tcgen05.ld is warp-collective); each lane re-filters
         // its row with its current threshold, and a pair that can enter the top-2 gets its
@@ -619,6 +649,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         while (wm) {
           const int gidx = __ffs(wm) - 1;
           wm &= wm - 1;
+          if (p.trace && lane == 0) atomicAdd((unsigned long long*)(p.trace + 8 * 256 * 2 + 2), 1ull);
           float w[8];
           tmem_ld8(lane_base + a * TILE + gidx * 8, w);
 #pragma unroll
@@ -629,6 +660,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
             if (cj < 0 || cj == ci) continue;
             if (!(lower_key(__fmaf_rn(-2.f, w[u], r), Erow, eta_row) <= T)) continue;
             const int64_t gj = (int64_t)J * TILE + j;
+            if (p.trace) atomicAdd((unsigned long long*)(p.trace + 8 * 256 * 2), 1ull);
             const float L = float_down(exact_dist<EUCLIDEAN>(p.X64 + g * d, p.X64 + gj * d, d));
             if (!(L <= T)) continue;  // cannot enter the top-2 (T: second best, global, dmax)
             const unsigned long long key = ((unsigned long long)__float_as_uint(L) << 32) | (unsigned)gj;
@@ -639,7 +671,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
               } else {
                 k2 = key;
               }
-              T = fminf(fminf(key_value(k2), gT), p.thr_hi);
+              T = fminf(fminf(key_value(k2), fminf(gT, tup)), p.thr_hi);
               gam = gamma_of(T);
             }
           }

@@ -3,7 +3,7 @@ import sys
 cur = None
 for line in open(sys.argv[1]):
     if line.startswith("launch"):
-        cur = line.split()[2]
+        cur = " ".join(line.split()[2:])
         rows = []
         continue
     f = line.split()
