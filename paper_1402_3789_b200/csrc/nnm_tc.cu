@@ -641,9 +641,12 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
           }
         }
         // exact insert path (rare): the warp re-reads only the 8-column groups where some
-        // lane may hold a candidate (tcgen05.ld is warp-collective); each lane re-filters
-        // its row with its current threshold, and a pair that can enter the top-2 gets its
-        // exact scipy-order FP64 value (rounded down) as key
+        // lane may hold a candidate (tcgen05.ld is warp-collective) and each lane marks its
+        // candidates (value, component and rigorous lower bound checks) in a 128-bit mask;
+        // then the lanes evaluate their candidates in lockstep -- each iteration every lane
+        // takes its next one -- so FP64 gather latencies are paid per candidate of the
+        // busiest lane, not per column position.  A candidate gets its exact scipy-order
+        // FP64 value (rounded down) as key.
         uint32_t wm = __reduce_or_sync(0xFFFFFFFFu, gm);
 #pragma unroll 1
         while (wm) {
@@ -652,14 +655,22 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
           if (p.trace && lane == 0) atomicAdd((unsigned long long*)(p.trace + 8 * 256 * 2 + 2), 1ull);
           float w[8];
           tmem_ld8(lane_base + a * TILE + gidx * 8, w);
+          uint32_t m8 = 0;
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             if (ci < 0 || !(w[u] >= gam)) continue;
-            const int j = gidx * 8 + u;
-            const int cj = S.bcomp[s][j];
+            const int cj = S.bcomp[s][gidx * 8 + u];
             if (cj < 0 || cj == ci) continue;
             if (!(lower_key(__fmaf_rn(-2.f, w[u], r), Erow, eta_row) <= T)) continue;
-            const int64_t gj = (int64_t)J * TILE + j;
+            m8 |= 1u << u;
+          }
+          // lockstep: each iteration every lane evaluates its next candidate of the group
+#pragma unroll 1
+          while (__any_sync(0xFFFFFFFFu, m8 != 0u)) {
+            if (m8 == 0u) continue;
+            const int u = __ffs(m8) - 1;
+            m8 &= m8 - 1;
+            const int64_t gj = (int64_t)J * TILE + gidx * 8 + u;
             if (p.trace) atomicAdd((unsigned long long*)(p.trace + 8 * 256 * 2), 1ull);
             const float L = float_down(exact_dist<EUCLIDEAN>(p.X64 + g * d, p.X64 + gj * d, d));
             if (!(L <= T)) continue;  // cannot enter the top-2 (T: second best, global, dmax)
