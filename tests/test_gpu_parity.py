@@ -274,3 +274,19 @@ def test_round_path_reuse_equals_full_rescans():
         outs.append(p.stdout.split())
     assert outs[0][0] == outs[1][0] and outs[0][1] == outs[1][1]
     assert int(outs[0][1]) > 20  # a multi-round run that exercised the reuse
+
+
+@pytest.mark.parametrize("d", [29, 30, 48])
+def test_high_dimension_paths_vs_oracle(nnm, d):
+    """d <= 29 runs the tensor-core scan, d > 29 the FP32 dot-form scan: both exact."""
+    from oracle import nnm_oracle as orc
+
+    X = nnm.generate_synthetic(2500, d, 11, 1.5, seed=d)[0]
+    X = X[np.random.default_rng(d).permutation(len(X))]
+    res = nnm.fit(X)
+    assert (res.device_stats["tc_items"] > 0) == (d <= 29)
+    m_or, a_or = orc.single_linkage(X)
+    got = _records(res.merges)
+    for f in FIELDS:
+        assert np.array_equal(got[f], m_or[f]), (d, f)
+    assert np.array_equal(res.assignments, a_or)
