@@ -671,76 +671,122 @@ __global__ void tc_items_kernel(const unsigned long long* __restrict__ keys, con
 // that can hold a cross-component pair with I (every pair of I x J in one
 // component is useless).  Seeds the component upper bounds.
 constexpr int PK = 8;
+// Tile-level passes handle TR row tiles per block: every column-tile centre is read once
+// and compared with the TR row centres (same fp32 operation order as cdist32).
+constexpr int TR = 8;
+
+template <int M>
+__device__ __forceinline__ void cdist32_rows(const float* __restrict__ c32, int T,
+                                             const float (*ci)[192], int J, int d,
+                                             float (&out)[TR]) {
+  float acc[TR];
+#pragma unroll
+  for (int r = 0; r < TR; ++r) acc[r] = 0.f;
+  for (int k = 0; k < d; ++k) {
+    const float cj = __ldg(c32 + (int64_t)k * T + J);
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const float t = fabsf(ci[r][k] - cj);
+      if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc[r] = fmaf(t, t, acc[r]);
+      else if (M == MANHATTAN) acc[r] += t;
+      else acc[r] = fmaxf(acc[r], t);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < TR; ++r) out[r] = (M == EUCLIDEAN || M == SQEUCLIDEAN) ? sqrtf(acc[r]) : acc[r];
+}
+
 template <int M>
 __global__ void phase1_kernel(const float* __restrict__ c32, const float* __restrict__ r32,
                               const int2* __restrict__ trange, int T, int d, int2* __restrict__ out) {
-  const int I = blockIdx.x;
-  __shared__ float ci[256];
-  for (int k = threadIdx.x; k < d; k += blockDim.x) ci[k] = c32[(int64_t)k * T + I];
+  const int I0 = blockIdx.x * TR;
+  const int nr = min(TR, T - I0);
+  __shared__ float ci[TR][192];
+  for (int t = threadIdx.x; t < TR * d; t += blockDim.x) {
+    const int r = t / d, k = t % d;
+    ci[r][k] = r < nr ? c32[(int64_t)k * T + I0 + r] : 0.f;
+  }
   __syncthreads();
-  double bl[2] = {INFINITY, INFINITY};
-  int bj[2] = {-1, -1};
+  double bl[TR][2];
+  int bj[TR][2];
+#pragma unroll
+  for (int r = 0; r < TR; ++r) {
+    bl[r][0] = bl[r][1] = INFINITY;
+    bj[r][0] = bj[r][1] = -1;
+  }
   for (int J = threadIdx.x; J < T; J += blockDim.x) {
-    if (same_single(trange, I, J)) continue;
-    // rank by distance from I's centre to J's ball (the tile itself first): the
-    // LB alone ties at 0 for every overlapping ball.  A heuristic seed order (any
-    // choice is sound): fp32, deterministic (ties by J)
-    double lb = (J == I) ? -INFINITY : (double)(cdist32<M>(c32, T, ci, J, d) - r32[J]);
-    if (lb < bl[1] || (lb == bl[1] && J < bj[1])) {
-      if (lb < bl[0] || (lb == bl[0] && J < bj[0])) {
-        bl[1] = bl[0]; bj[1] = bj[0]; bl[0] = lb; bj[0] = J;
-      } else {
-        bl[1] = lb; bj[1] = J;
+    float dc[TR];
+    cdist32_rows<M>(c32, T, ci, J, d, dc);
+    const float rJ = r32[J];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int I = I0 + r;
+      if (r >= nr || same_single(trange, I, J)) continue;
+      // rank by distance from I's centre to J's ball (the tile itself first): the
+      // LB alone ties at 0 for every overlapping ball.  A heuristic seed order (any
+      // choice is sound): fp32, deterministic (ties by J)
+      const double lb = (J == I) ? -INFINITY : (double)(dc[r] - rJ);
+      if (lb < bl[r][1] || (lb == bl[r][1] && J < bj[r][1])) {
+        if (lb < bl[r][0] || (lb == bl[r][0] && J < bj[r][0])) {
+          bl[r][1] = bl[r][0]; bj[r][1] = bj[r][0]; bl[r][0] = lb; bj[r][0] = J;
+        } else {
+          bl[r][1] = lb; bj[r][1] = J;
+        }
       }
     }
   }
   __shared__ double sl[512];
   __shared__ int sj[512];
-  sl[2 * threadIdx.x] = bl[0]; sj[2 * threadIdx.x] = bj[0];
-  sl[2 * threadIdx.x + 1] = bl[1]; sj[2 * threadIdx.x + 1] = bj[1];
-  __syncthreads();
-  // PK rounds of block arg-min over the 512 candidates (tiny)
   __shared__ double rl[8];
   __shared__ int ri[8];
-  for (int k = 0; k < PK; ++k) {
-    double v = INFINITY;
-    int at = -1;
-    for (int c = threadIdx.x; c < 2 * blockDim.x; c += blockDim.x) {
-      if (sj[c] >= 0 && (sl[c] < v || (sl[c] == v && (at < 0 || sj[c] < sj[at])))) {
-        v = sl[c];
-        at = c;
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      double ov = __shfl_xor_sync(0xFFFFFFFFu, v, o);
-      int oa = __shfl_xor_sync(0xFFFFFFFFu, at, o);
-      if (oa >= 0 && (at < 0 || ov < v || (ov == v && sj[oa] < sj[at]))) {
-        v = ov;
-        at = oa;
-      }
-    }
-    if ((threadIdx.x & 31) == 0) {
-      rl[threadIdx.x >> 5] = v;
-      ri[threadIdx.x >> 5] = at;
-    }
+#pragma unroll
+  for (int r = 0; r < TR; ++r) {
+    if (r >= nr) break;  // uniform per block
+    const int I = I0 + r;
+    sl[2 * threadIdx.x] = bl[r][0]; sj[2 * threadIdx.x] = bj[r][0];
+    sl[2 * threadIdx.x + 1] = bl[r][1]; sj[2 * threadIdx.x + 1] = bj[r][1];
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double bv = INFINITY;
-      int ba = -1;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-        if (ri[w] >= 0 && (ba < 0 || rl[w] < bv || (rl[w] == bv && sj[ri[w]] < sj[ba]))) {
-          bv = rl[w];
-          ba = ri[w];
+    // PK rounds of block arg-min over the 512 candidates (tiny)
+    for (int k = 0; k < PK; ++k) {
+      double v = INFINITY;
+      int at = -1;
+      for (int c = threadIdx.x; c < 2 * blockDim.x; c += blockDim.x) {
+        if (sj[c] >= 0 && (sl[c] < v || (sl[c] == v && (at < 0 || sj[c] < sj[at])))) {
+          v = sl[c];
+          at = c;
         }
-      int2 it = make_int2(-1, -1);
-      if (ba >= 0) {
-        int J = sj[ba];
-        it = make_int2(min(I, J), max(I, J));
-        sj[ba] = -1;  // remove
       }
-      out[(int64_t)I * PK + k] = it;
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        int oa = __shfl_xor_sync(0xFFFFFFFFu, at, o);
+        if (oa >= 0 && (at < 0 || ov < v || (ov == v && sj[oa] < sj[at]))) {
+          v = ov;
+          at = oa;
+        }
+      }
+      if ((threadIdx.x & 31) == 0) {
+        rl[threadIdx.x >> 5] = v;
+        ri[threadIdx.x >> 5] = at;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double bv = INFINITY;
+        int ba = -1;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+          if (ri[w] >= 0 && (ba < 0 || rl[w] < bv || (rl[w] == bv && sj[ri[w]] < sj[ba]))) {
+            bv = rl[w];
+            ba = ri[w];
+          }
+        int2 it = make_int2(-1, -1);
+        if (ba >= 0) {
+          int J = sj[ba];
+          it = make_int2(min(I, J), max(I, J));
+          sj[ba] = -1;  // remove
+        }
+        out[(int64_t)I * PK + k] = it;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
@@ -794,32 +840,47 @@ __global__ void enum_count_kernel(const float* __restrict__ c32, const float* __
                                   const int2* __restrict__ trange, const double* __restrict__ umax,
                                   const unsigned* __restrict__ bits, int T, int d,
                                   unsigned char* __restrict__ keep, int* __restrict__ counts) {
-  const int I = blockIdx.x;
-  __shared__ float ci[256];
-  for (int k = threadIdx.x; k < d; k += blockDim.x) ci[k] = c32[(int64_t)k * T + I];
-  __syncthreads();
-  const double uI = umax[I];
-  const float cnI = cn[I], rI = r32[I];
-  int c = 0;
-  const int64_t w0 = tri_index(T, I, I);
-  for (int J = I + threadIdx.x; J < T; J += blockDim.x) {
-    const int64_t w = w0 + (J - I);
-    bool k = !((bits[w >> 5] >> (w & 31)) & 1u) && !same_single(trange, I, J);
-    // kept iff the rigorous lower bound of the tile pair can reach either component
-    // bound (a kept superset costs work, never exactness)
-    if (k && J != I) k = tile_lb32<M>(cdist32<M>(c32, T, ci, J, d), cnI, cn[J], rI, r32[J], d) <=
-                         fmax(uI, umax[J]);
-    keep[w] = k;
-    c += k;
+  const int I0 = blockIdx.x * TR;
+  const int nr = min(TR, T - I0);
+  __shared__ float ci[TR][192];
+  for (int t = threadIdx.x; t < TR * d; t += blockDim.x) {
+    const int r = t / d, k = t % d;
+    ci[r][k] = r < nr ? c32[(int64_t)k * T + I0 + r] : 0.f;
   }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  __shared__ int s[8];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  int c[TR];
+#pragma unroll
+  for (int r = 0; r < TR; ++r) c[r] = 0;
+  for (int J = I0 + threadIdx.x; J < T; J += blockDim.x) {
+    float dc[TR];
+    cdist32_rows<M>(c32, T, ci, J, d, dc);
+    const double uJ = umax[J];
+    const float cnJ = cn[J], rJ = r32[J];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int I = I0 + r;
+      if (r >= nr || J < I) continue;
+      const int64_t w = tri_index(T, I, J);
+      bool k = !((bits[w >> 5] >> (w & 31)) & 1u) && !same_single(trange, I, J);
+      // kept iff the rigorous lower bound of the tile pair can reach either component
+      // bound (a kept superset costs work, never exactness)
+      if (k && J != I) k = tile_lb32<M>(dc[r], cn[I], cnJ, r32[I], rJ, d) <= fmax(umax[I], uJ);
+      keep[w] = k;
+      c[r] += k;
+    }
+  }
+  __shared__ int s[TR][8];
+#pragma unroll
+  for (int r = 0; r < TR; ++r) {
+    int v = c[r];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) s[r][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nr) {
     int t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
-    counts[I] = t;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[threadIdx.x][w];
+    counts[I0 + threadIdx.x] = t;
   }
 }
 
@@ -848,14 +909,6 @@ __global__ void enum_write_kernel(const unsigned char* __restrict__ keep,
     base += tot;
     __syncthreads();
   }
-}
-
-__global__ void count_diag_kernel(const int2* __restrict__ items, int64_t cnt,
-                                  unsigned long long* acc) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned v = (t < cnt && items[t].x == items[t].y) ? 1u : 0u;
-  v = __reduce_add_sync(0xFFFFFFFFu, v);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(acc, (unsigned long long)v);
 }
 
 __global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt,
@@ -1834,7 +1887,7 @@ struct nnm_dataset {
     const int64_t W = tile_pairs();
     // phase-1 seeds: PK nearest cross-capable tiles per tile
     items1.ensure((size_t)Tp * PK);
-    phase1_kernel<M><<<Tp, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
+    phase1_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     auto* k64 = reinterpret_cast<unsigned long long*>(items1.p);  // (I, J) -> J << 32 | I order
     // sort by (I, J): int2 memory is {x=I, y=J}; as u64 little-endian = J << 32 | I -> swap to key
@@ -1862,7 +1915,7 @@ struct nnm_dataset {
     pkeep.ensure(W);
     pcount.ensure(Tp);
     poffset.ensure(Tp + 1);
-    enum_count_kernel<M><<<Tp, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
+    enum_count_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
                                              Tp, d, pkeep.p, pcount.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), pcount.p, pcount.p + Tp, poffset.p, 0LL);

@@ -776,14 +776,6 @@ __global__ void tc_tile_max_kernel(const float* __restrict__ tnorm, const float*
   }
 }
 
-__global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n, int2* __restrict__ out) {
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= n) return;
-  const int2 it = items[w];
-  out[2 * w] = it;
-  out[2 * w + 1] = (it.x != it.y) ? make_int2(it.y, it.x) : make_int2(0x7FFFFFFF, 0x7FFFFFFF);
-}
-
 // Error-model probe: for dumped accumulators of `items`, compare the rigorous key L
 // and the bound with the exact scipy-order FP64 value S of every real, distinct pair.
 // out[0] = max |v - S| / bound (atomicMax on the bits of a nonnegative float),
@@ -881,10 +873,5 @@ cudaError_t launch_tc_prepare(const double* X64p, const int* porig, const double
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_mirror(const int2* items, int64_t n, int2* out, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  tc_mirror_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(items, n, out);
-  return cudaGetLastError();
-}
 
 }  // namespace nnm

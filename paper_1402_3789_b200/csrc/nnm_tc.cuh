@@ -46,8 +46,6 @@ cudaError_t launch_tc_prepare(const double* X64p, const int* porig, const double
 cudaError_t launch_tc_probe(const TcArgs& a, const double* X64p, const int2* items, int64_t n,
                             unsigned long long* out, cudaStream_t st);
 
-// Full-square item list: out[2w] = items[w], out[2w+1] = mirrored (J, I), or the sentinel
-// (INT_MAX, INT_MAX) for a diagonal item (it sorts last; the caller sorts by (I, J)).
-cudaError_t launch_tc_mirror(const int2* items, int64_t n, int2* out, cudaStream_t st);
+
 
 }  // namespace nnm
