@@ -174,6 +174,12 @@ int nnm_csv_load(const char *path, char delimiter, const char *id_column, int32_
 int nnm_csv_fetch(nnm_csv *table, double *values, char *id_buf, int64_t *id_offsets);
 int nnm_csv_free(nnm_csv *table);
 
+/* ---- Dataset validation (model.py:29-76) ----
+ * Index of the first non-finite element of count float64 values (-1 if all are
+ * finite); the Dataset constructor turns it into "non-finite feature value in
+ * row r".  Host-only, multi-threaded (threads <= 0: every core). */
+int nnm_first_nonfinite(const double *X, int64_t count, int32_t threads, int64_t *out_index);
+
 /* ---- diagnostics ----
  * Sustained FP32 (FFMA2) throughput of `device` in TFLOP/s: the roofline
  * denominator for the screening scan, which runs on the FP32 pipe. */

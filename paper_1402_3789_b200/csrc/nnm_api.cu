@@ -45,6 +45,7 @@ void nnm_csv_copy_values(const nnm_csv* c, double* out);
 int64_t nnm_csv_id_bytes(const nnm_csv* c);
 void nnm_csv_copy_ids(const nnm_csv* c, char* buf, int64_t* offsets);
 void nnm_csv_destroy(nnm_csv* c);
+int64_t nnm_first_nonfinite_impl(const double* x, int64_t count, int threads);
 
 using namespace nnm;
 
@@ -117,23 +118,55 @@ struct DevBuf {
   }
 };
 
+// Page-locked host blocks are recycled process-wide: cudaMallocHost / cudaFreeHost
+// cost milliseconds to seconds (page pinning, implicit device sync), and the
+// reference-facing API creates one dataset per user call.
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;
+  void* get(size_t& bytes) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_blocks.lower_bound(bytes);
+      if (it != free_blocks.end()) {
+        bytes = it->first;
+        void* p = it->second;
+        free_blocks.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    CUDA_TRY(cudaMallocHost(&p, bytes));
+    return p;
+  }
+  void put(void* p, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    free_blocks.emplace(bytes, p);
+  }
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* pool = new PinnedPool();  // never destroyed: outlives every dataset
+  return *pool;
+}
+
 template <class T>
-struct PinnedBuf {  // grow-only page-locked host staging buffer
+struct PinnedBuf {  // grow-only page-locked host staging buffer (blocks from pinned_pool)
   T* p = nullptr;
-  size_t n = 0;
+  size_t n = 0, bytes = 0;
   PinnedBuf() = default;
   PinnedBuf(const PinnedBuf&) = delete;
   PinnedBuf& operator=(const PinnedBuf&) = delete;
   ~PinnedBuf() {
-    if (p) cudaFreeHost(p);
+    if (p) pinned_pool().put(p, bytes);
   }
   T* ensure(size_t count) {
     if (count <= n && p) return p;
-    if (p) cudaFreeHost(p);
+    if (p) pinned_pool().put(p, bytes);
     p = nullptr;
     n = 0;
-    CUDA_TRY(cudaMallocHost((void**)&p, std::max<size_t>(count, 1) * sizeof(T)));
-    n = count;
+    bytes = std::max<size_t>(count, 1) * sizeof(T);
+    p = (T*)pinned_pool().get(bytes);
+    n = bytes / sizeof(T);
     return p;
   }
 };
@@ -1266,8 +1299,11 @@ struct CachedAlloc {
       free_blocks.erase(it);
       return p;
     }
+    // from the stream-ordered pool (release threshold raised): a new dataset reuses
+    // the pool's pages instead of cudaMalloc / device-synchronising cudaFree
     char* p = nullptr;
-    CUDA_TRY(cudaMalloc(&p, (size_t)n));
+    s = t_alloc_stream;
+    CUDA_TRY(cudaMallocAsync((void**)&p, (size_t)n, s));
     used[p] = (size_t)n;
     return p;
   }
@@ -1276,9 +1312,10 @@ struct CachedAlloc {
     free_blocks.emplace(it->second, p);
     used.erase(it);
   }
+  cudaStream_t s = nullptr;
   void release() {
-    for (auto& kv : free_blocks) cudaFree(kv.second);
-    for (auto& kv : used) cudaFree(kv.first);
+    for (auto& kv : free_blocks) cudaFreeAsync(kv.second, s);
+    for (auto& kv : used) cudaFreeAsync(kv.first, s);
     free_blocks.clear();
     used.clear();
   }
@@ -2405,6 +2442,14 @@ int nnm_csv_fetch(nnm_csv* c, double* values, char* id_buf, int64_t* id_offsets)
 
 int nnm_csv_free(nnm_csv* c) {
   return guarded([&] { nnm_csv_destroy(c); });
+}
+
+int nnm_first_nonfinite(const double* X, int64_t count, int32_t threads, int64_t* out_index) {
+  return guarded([&] {
+    if ((!X && count > 0) || !out_index) invalid("null argument");
+    if (count < 0) invalid("negative count");
+    *out_index = count > 0 ? nnm_first_nonfinite_impl(X, count, threads) : -1;
+  });
 }
 
 int nnm_dataset_destroy(nnm_dataset* ds) {
