@@ -1327,7 +1327,12 @@ struct CachedAlloc {
 struct StreamHolder {
   cudaStream_t st = nullptr;
   ~StreamHolder() {
-    if (st) cudaStreamDestroy(st);
+    // the members' cudaFreeAsync calls are queued on st by now: let them complete so
+    // the pool can hand the pages straight to the next dataset (no pool growth)
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
   }
 };
 
@@ -2324,11 +2329,27 @@ void init_device(int32_t device, int* sms) {
     throw NnmError{NNM_E_CUDA, "no CUDA device available (libnnm has no CPU fallback)"};
   if (device < 0 || device >= count) invalid("device index out of range");
   CUDA_TRY(cudaSetDevice(device));
+  // device properties and the pool setting once per device (cudaGetDeviceProperties
+  // queries every attribute: too slow for a per-call path)
+  static std::mutex mu;
+  static std::map<int, int> known_sms;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = known_sms.find(device);
+    if (it != known_sms.end()) {
+      *sms = it->second;
+      return;
+    }
+  }
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   if (prop.major < 10)
     throw NnmError{NNM_E_CUDA, std::string("libnnm is built for sm_100a; device is ") + prop.name};
   *sms = prop.multiProcessorCount;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    known_sms[device] = prop.multiProcessorCount;
+  }
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t keep = UINT64_MAX;
@@ -2358,6 +2379,7 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
     CUDA_TRY(cudaEventCreate(&ds->ev1));
     if ((size_t)ds->d * TILE * 2 * sizeof(float) + 8192 > 200 * 1024)
       throw NnmError{NNM_E_UNSUPPORTED, "d too large for the shared-memory tile (d <= 190)"};
+    auto tc0 = std::chrono::steady_clock::now();
     ds->X64.ensure((size_t)n * d);
     CUDA_TRY(cudaMemcpyAsync(ds->X64.p, X, (size_t)n * d * sizeof(double),
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ds->st));
@@ -2373,6 +2395,9 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
     unsigned long long h[2];
     CUDA_TRY(cudaMemcpyAsync(h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, ds->st));
     ds->sync();
+    if (getenv("NNM_DEBUG"))
+      fprintf(stderr, "[nnm] dataset create: alloc+upload+prepare %.2f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tc0).count());
     if (h[0] != ~0ull) invalid("non-finite feature value in row " + std::to_string(h[0] + 1));
     if (h[1])
       throw NnmError{NNM_E_UNSUPPORTED,

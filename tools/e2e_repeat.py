@@ -9,6 +9,8 @@ from paper_1402_3789_b200.datagen import config_dataset
 from paper_1402_3789_b200.engine import run_arrays
 X = config_dataset(sys.argv[1] if len(sys.argv) > 1 else "c4")
 Xh = torch.from_numpy(X).pin_memory().numpy()
+if os.environ.get("NOGC"):
+    gc.disable()
 for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 6):
     t = [time.perf_counter()]
     ds = nnm.Dataset(values=Xh); t.append(time.perf_counter())
