@@ -656,7 +656,8 @@ __device__ __forceinline__ double tile_lb32(float dc, float cnI, float cnJ, floa
 __global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n,
                                  const double* __restrict__ umax, const float* __restrict__ c32,
                                  const float* __restrict__ cn, const float* __restrict__ r32, int T,
-                                 int d, int metric, unsigned long long* __restrict__ keys,
+                                 int d, int metric, const unsigned* __restrict__ tpmin,
+                                 unsigned long long* __restrict__ keys,
                                  int* __restrict__ js, unsigned long long* __restrict__ dropped) {
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned drop = 0;
@@ -679,6 +680,11 @@ __global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n,
         lb = tile_lb32<EUCLIDEAN>(dc, cn[it.x], cn[it.y], r32[it.x], r32[it.y], d);
       }
       if (umax) {
+        if (tpmin) {  // the bound enum_count_kernel applied (items are (I <= J))
+          const int lo = min(it.x, it.y), hi = max(it.x, it.y);
+          const int64_t w2 = (int64_t)lo * T - (int64_t)lo * (lo - 1) / 2 + (hi - lo);
+          lb = fmax(lb, (double)__uint_as_float(tpmin[w2]));
+        }
         keep_ij = lb <= umax[it.x];
         keep_ji = lb <= umax[it.y];
       }
@@ -872,6 +878,7 @@ __global__ void enum_count_kernel(const float* __restrict__ c32, const float* __
                                   const float* __restrict__ r32,
                                   const int2* __restrict__ trange, const double* __restrict__ umax,
                                   const unsigned* __restrict__ bits, int T, int d,
+                                  const unsigned* __restrict__ tpmin,
                                   unsigned char* __restrict__ keep, int* __restrict__ counts) {
   const int I0 = blockIdx.x * TR;
   const int nr = min(TR, T - I0);
@@ -897,7 +904,11 @@ __global__ void enum_count_kernel(const float* __restrict__ c32, const float* __
       bool k = !((bits[w >> 5] >> (w & 31)) & 1u) && !same_single(trange, I, J);
       // kept iff the rigorous lower bound of the tile pair can reach either component
       // bound (a kept superset costs work, never exactness)
-      if (k && J != I) k = tile_lb32<M>(dc[r], cn[I], cnJ, r32[I], rJ, d) <= fmax(umax[I], uJ);
+      if (k && J != I) {
+        double lb = tile_lb32<M>(dc[r], cn[I], cnJ, r32[I], rJ, d);
+        if (tpmin) lb = fmax(lb, (double)__uint_as_float(tpmin[w]));  // scanned before: its bound
+        k = lb <= fmax(umax[I], uJ);
+      }
       keep[w] = k;
       c[r] += k;
     }
@@ -1409,6 +1420,11 @@ struct nnm_dataset {
   DevBuf<double> tcenter, tradius, tumax;
   DevBuf<float> tc32, tcn32, tr32;  // fp32 SoA tile centres / norms / radii (tile passes)
   DevBuf<int2> items1, items2;
+  // per tile pair (triangle index): fp32 bits of a lower bound of S over its cross-component
+  // pairs, written by the tensor-core scan, read by the phase-2 enumeration (0: unknown)
+  DevBuf<unsigned> tpmin;
+  bool tpmin_on = false;   // allocated and reset for this run
+  bool tpmin_use = false;  // this scan may read / write it (single-rank scans only)
   DevBuf<unsigned> pbits;
   DevBuf<unsigned char> pkeep;
   DevBuf<int> pcount;
@@ -1604,7 +1620,9 @@ struct nnm_dataset {
     tc_keys.ensure((size_t)2 * n_up);
     tc_js.ensure((size_t)2 * n_up);
     tc_mirror_kernel<<<blocks_for(n_up), 256, 0, st>>>(items + w_begin, n_up, umax, tc32.p, tcn32.p,
-                                                       tr32.p, Tp, d, bv_metric, tc_keys.p, tc_js.p,
+                                                       tr32.p, Tp, d, bv_metric,
+                                                       (umax && tpmin_use) ? tpmin.p : nullptr,
+                                                       tc_keys.p, tc_js.p,
                                                        counters.p + 5); note_launch();
     CUDA_TRY(cudaGetLastError());
     thrust::sort_by_key(thrust::cuda::par(talloc).on(st), tc_keys.p, tc_keys.p + 2 * n_up, tc_js.p);
@@ -1630,6 +1648,7 @@ struct nnm_dataset {
     a.B1 = b1;
     a.B2 = b2;
     a.dump = nullptr;
+    a.tpmin = tpmin_use ? tpmin.p : nullptr;
     const char* dbg = getenv("NNM_TC_DBG");
     a.dbg = dbg ? atoi(dbg) : 0;
     const int grid = (int)std::min<int64_t>(nfull, (int64_t)sms);
@@ -1789,6 +1808,14 @@ struct nnm_dataset {
     edges.ensure(std::max<int64_t>(n - 1, 1));
     flag.ensure(1);
     CUDA_TRY(cudaMemsetAsync(counters.p, 0, 8 * sizeof(unsigned long long), st));
+    // tile-pair bound cache (TC scan only; 4 B per tile pair: 0.58 GB at 2M points)
+    const char* ce = getenv("NNM_TPCACHE");
+    tpmin_use = false;
+    tpmin_on = tc_on && !(ce && ce[0] == '0') && tile_pairs() * 4 <= ((int64_t)4 << 30);
+    if (tpmin_on) {
+      tpmin.ensure(tile_pairs());
+      CUDA_TRY(cudaMemsetAsync(tpmin.p, 0, tile_pairs() * sizeof(unsigned), st));
+    }
     bv_round = 0;
     bv_ncomp = n;
   }
@@ -1958,7 +1985,8 @@ struct nnm_dataset {
     pcount.ensure(Tp);
     poffset.ensure(Tp + 1);
     enum_count_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
-                                             Tp, d, pkeep.p, pcount.p); note_launch();
+                                             Tp, d, tpmin_use ? tpmin.p : nullptr,
+                                             pkeep.p, pcount.p); note_launch();
     CUDA_TRY(cudaGetLastError());
     thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), pcount.p, pcount.p + Tp, poffset.p, 0LL);
     long long last_off = read1(poffset.p + (Tp - 1));
@@ -1985,6 +2013,9 @@ struct nnm_dataset {
   void pruned_scan_shard(int metric, unsigned long long* b1, unsigned long long* b2, int rank,
                          int world) {
     ensure_geometry(metric);
+    // every rank must derive the same phase-2 list without an exchange: the cache holds
+    // rank-local bounds, so only a single-rank scan reads or writes it
+    tpmin_use = tpmin_on && world == 1;
     tile_range.ensure(Tp);
     tile_range_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, Tp, tile_range.p); note_launch();
     int64_t n1 = 0, n2 = 0;

@@ -79,6 +79,8 @@ struct TcSmem {
   int ringrt[TC_RING];                 // row-tile index of item q, negated-minus-one when item q
                                        // is the first of its row tile (producer)
   int slot[2][8];
+  unsigned lbw[TC_EPI_GROUPS][2][4];   // tile-pair bound: per-quadrant minima of an item
+  int lbcnt[TC_EPI_GROUPS][2];         // (epilogue group, item parity) arrivals
   unsigned long long full[TC_STAGES], prepped[TC_STAGES], empty[TC_STAGES];
   unsigned long long tfull[TC_ACC], tempty[TC_ACC], afull[2], aprepped[2], aempty[2];
   uint32_t tmem_base;
@@ -372,6 +374,8 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
       mbar_init(&S.aprepped[a], 1);
       mbar_init(&S.aempty[a], 1);
     }
+    for (int g = 0; g < TC_EPI_GROUPS; ++g)
+      for (int b = 0; b < 2; ++b) S.lbcnt[g][b] = 0;
     fence_barrier_init();
   }
   if (warp == TC_MMA_WARP) {
@@ -591,6 +595,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         // fast filter, 64 columns at a time: maxima of the 8-column groups (the first
         // levels of the reduction tree) -> bit mask of groups that may hold a candidate
         uint32_t gm = 0;
+        float rmax = -INFINITY;  // largest G' of the row (tile-pair bound)
 #pragma unroll 1
         for (int hb = 0; hb < 2; ++hb) {
           float v[64];
@@ -605,6 +610,8 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
             for (int k = 0; k < 8; ++k)
               g8[k] = fmaxf(fmaxf(fmaxf(v[8 * k], v[8 * k + 1]), fmaxf(v[8 * k + 2], v[8 * k + 3])),
                             fmaxf(fmaxf(v[8 * k + 4], v[8 * k + 5]), fmaxf(v[8 * k + 6], v[8 * k + 7])));
+            rmax = fmaxf(rmax, fmaxf(fmaxf(fmaxf(g8[0], g8[1]), fmaxf(g8[2], g8[3])),
+                                     fmaxf(fmaxf(g8[4], g8[5]), fmaxf(g8[6], g8[7]))));
             uint32_t m = 0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) m |= (g8[k] >= gam) ? (1u << k) : 0u;
@@ -684,6 +691,29 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
               }
               T = fminf(fminf(key_value(k2), fminf(gT, tup)), p.thr_hi);
               gam = gamma_of(T);
+            }
+          }
+        }
+        // tile-pair lower bound (DESIGN 3.1): min over the item's rows of L(r_i - 2 max_j G'),
+        // a rigorous lower bound of S over every pair not masked as same-component now,
+        // hence of every cross-component pair in later rounds.  The 4 quadrant warps
+        // combine through shared memory (the last to arrive publishes with atomicMax:
+        // both orientations and all rounds give valid bounds, the largest is kept).
+        if (p.tpmin && !p.dump) {
+          const float lbr = ci >= 0 ? lower_key(__fmaf_rn(-2.f, rmax, r), Erow, eta_row) : INFINITY;
+          const unsigned mw = __reduce_min_sync(0xFFFFFFFFu, __float_as_uint(lbr));
+          if (lane == 0) {
+            const int par = (q / TC_EPI_GROUPS) & 1;
+            volatile unsigned* lw = S.lbw[e][par];
+            lw[warp & 3] = mw;
+            __threadfence_block();
+            if (atomicAdd(&S.lbcnt[e][par], 1) == 3) {
+              __threadfence_block();
+              const unsigned mm = min(min(lw[0], lw[1]), min(lw[2], lw[3]));
+              S.lbcnt[e][par] = 0;
+              const int lo = min(I, J), hi = max(I, J);
+              const int64_t w = (int64_t)lo * p.T - (int64_t)lo * (lo - 1) / 2 + (hi - lo);
+              if (mm != 0u) atomicMax(p.tpmin + w, mm);
             }
           }
         }

@@ -30,6 +30,8 @@ struct TcArgs {
   unsigned long long* B2; // [np] second-best key
   float* dump;            // debug: raw accumulators [items][128][128] (nullptr in production)
   long long* trace;       // NNM_TC_TRACE: [5 roles][256 items][2] clock64 stamps of CTA 0
+  unsigned* tpmin;        // [T(T+1)/2] per tile pair: fp32 bits of a lower bound of S over
+                          // the pairs not masked same-component (atomicMax; nullptr: off)
   int dbg;                // timing experiments (NNM_TC_DBG): 1 = no epilogue work, 2 = no prep work
 };
 

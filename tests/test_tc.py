@@ -127,3 +127,24 @@ def test_tc_and_fp32_paths_identical_at_scale(nnm):
     b = _run_env(code, {"NNM_TC": "0"}).split()
     assert a[1] == "True" and b[1] == "False"
     assert a[0] == b[0]
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c3"])
+def test_tile_pair_bound_cache_identical_at_full_scale(nnm, cfg):
+    """BASELINE configs 4 (2M x 25 full dendrogram) and 3 (500k x 25, dmax=5): the
+    tile-pair lower-bound cache (phase-2 pairs pruned with bounds from earlier scans)
+    gives byte-identical merges and labels to the scan without it, and scans fewer
+    tile pairs."""
+    code = ("import hashlib, paper_1402_3789_b200 as nnm\n"
+            "from paper_1402_3789_b200.datagen import config_dataset\n"
+            f"X = config_dataset('{cfg}')\n"
+            f"r = nnm.fit(X, dmax={'5.0' if cfg == 'c3' else 'None'})\n"
+            "print(hashlib.sha256(r.merges.array.tobytes() + r.assignments.tobytes()).hexdigest(),"
+            " r.device_stats['tc_items'], len(r.merges))\n")
+    a = _run_env(code, {"NNM_TPCACHE": "1"}).split()
+    b = _run_env(code, {"NNM_TPCACHE": "0"}).split()
+    assert a[0] == b[0]
+    assert a[2] == b[2]
+    if cfg == "c4":
+        assert a[2] == "1999999"
+        assert int(a[1]) < int(b[1])
