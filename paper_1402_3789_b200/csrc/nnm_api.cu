@@ -762,9 +762,11 @@ __global__ void phase1_kernel(const float* __restrict__ c32, const float* __rest
       const int I = I0 + r;
       if (r >= nr || same_single(trange, I, J)) continue;
       // rank by distance from I's centre to J's ball (the tile itself first): the
-      // LB alone ties at 0 for every overlapping ball.  A heuristic seed order (any
-      // choice is sound): fp32, deterministic (ties by J)
-      const double lb = (J == I) ? -INFINITY : (double)(dc[r] - rJ);
+      // LB alone ties at 0 for every overlapping ball.  J's radius counts at most as
+      // much as I's own, so a wide tile (pieces of several clusters) cannot crowd the
+      // compact neighbours out of the PK slots.  A heuristic seed order (any choice
+      // is sound): fp32, deterministic (ties by J)
+      const double lb = (J == I) ? -INFINITY : (double)(dc[r] - fminf(rJ, r32[I]));
       if (lb < bl[r][1] || (lb == bl[r][1] && J < bj[r][1])) {
         if (lb < bl[r][0] || (lb == bl[r][0] && J < bj[r][0])) {
           bl[r][1] = bl[r][0]; bj[r][1] = bj[r][0]; bl[r][0] = lb; bj[r][0] = J;
@@ -981,11 +983,11 @@ __device__ __forceinline__ uint32_t f2ord(float f) {
 
 __global__ void kd_dim_kernel(const double* __restrict__ X64, int d, const int* __restrict__ order,
                               const int* __restrict__ sbeg, const int* __restrict__ ssz, int nseg,
-                              int* __restrict__ sdim) {
+                              int leaf_split, int* __restrict__ sdim) {
   const int sgm = blockIdx.x;
   if (sgm >= nseg) return;
   const int sz = ssz[sgm];
-  if (sz <= TILE) {
+  if (sz <= 1 || (sz <= TILE && !leaf_split)) {
     if (threadIdx.x == 0) sdim[sgm] = -1;
     return;
   }
@@ -1036,11 +1038,11 @@ __global__ void kd_key_kernel(const double* __restrict__ X64, int64_t n, int d,
 // multiple of 128 nearest the median.  Segments <= TILE are leaves.
 __global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
                                    const int* __restrict__ sbeg, const int* __restrict__ ssz,
-                                   int nseg, int* __restrict__ ssplit) {
+                                   int nseg, int allow_off, int* __restrict__ ssplit) {
   const int sgm = blockIdx.x;
   if (sgm >= nseg) return;
   const int sz = ssz[sgm], b = sbeg[sgm];
-  if (sz <= TILE) {
+  if (sz <= 1 || (sz <= TILE && !allow_off)) {
     if (threadIdx.x == 0) ssplit[sgm] = sz;
     return;
   }
@@ -1049,14 +1051,18 @@ __global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
     u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
     return __uint_as_float(u);
   };
-  const int lo = sz / 4, hi = sz - sz / 4;  // candidate cuts: left size in [lo, hi]
-  float bg = -1.f;
-  int bp = sz / 2;
-  for (int i = lo + threadIdx.x; i <= hi; i += blockDim.x) {
+  const int lo = sz / 4, hi = sz - sz / 4;  // balanced cuts: left size in [lo, hi]
+  float bg = -1.f, bg2 = -1.f;              // largest gap: balanced range / anywhere
+  int bp = sz / 2, bp2 = sz / 2;
+  for (int i = 1 + threadIdx.x; i < sz; i += blockDim.x) {
     const float g = val(i) - val(i - 1);
-    if (g > bg || (g == bg && i < bp)) {
+    if (i >= lo && i <= hi && (g > bg || (g == bg && i < bp))) {
       bg = g;
       bp = i;
+    }
+    if (g > bg2 || (g == bg2 && i < bp2)) {
+      bg2 = g;
+      bp2 = i;
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -1066,21 +1072,36 @@ __global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
       bg = og;
       bp = op;
     }
+    og = __shfl_xor_sync(0xFFFFFFFFu, bg2, o);
+    op = __shfl_xor_sync(0xFFFFFFFFu, bp2, o);
+    if (og > bg2 || (og == bg2 && op < bp2)) {
+      bg2 = og;
+      bp2 = op;
+    }
   }
   if (threadIdx.x == 0) {
+    const float ext = val(sz - 1) - val(0);
+    if (sz <= TILE) {
+      // a leaf that holds two separated groups (a piece of a neighbouring cluster) is
+      // split at the gap: one ball per group keeps the tile bounds tight
+      ssplit[sgm] = (sz >= 16 && ext > 0.f && bg2 >= 0.5f * ext) ? bp2 : sz;
+      return;
+    }
     // no real gap: cut at the multiple of 128 nearest the median, so compact
     // clusters fill whole tiles (few pad slots)
-    const float ext = val(sz - 1) - val(0);
     int L = ((sz + TILE) / (2 * TILE)) * TILE;
     if (L < TILE) L = TILE;
     if (L > sz - 1) L = sz - 1;
-    ssplit[sgm] = (ext > 0.f && bg >= 0.1f * ext) ? bp : L;
+    if (ext > 0.f && bg >= 0.1f * ext) L = bp;
+    else if (allow_off && ext > 0.f && bg2 >= 0.25f * ext) L = bp2;  // cut a separated piece off
+    ssplit[sgm] = L;
   }
 }
 
-__global__ void kd_children_kernel(int nseg, const int* __restrict__ ssz, int* __restrict__ nchild) {
+__global__ void kd_children_kernel(int nseg, const int* __restrict__ ssz,
+                                   const int* __restrict__ ssplit, int* __restrict__ nchild) {
   int sgm = blockIdx.x * blockDim.x + threadIdx.x;
-  if (sgm < nseg) nchild[sgm] = ssz[sgm] > TILE ? 2 : 1;
+  if (sgm < nseg) nchild[sgm] = ssplit[sgm] < ssz[sgm] ? 2 : 1;
 }
 
 __global__ void kd_newsegs_kernel(int nseg, const int* __restrict__ sbeg, const int* __restrict__ ssz,
@@ -1091,7 +1112,7 @@ __global__ void kd_newsegs_kernel(int nseg, const int* __restrict__ sbeg, const 
   const int c = cbase[sgm], sz = ssz[sgm], L = ssplit[sgm];
   nbeg[c] = sbeg[sgm];
   nsz[c] = L;
-  if (sz > TILE) {
+  if (L < sz) {
     nbeg[c + 1] = sbeg[sgm] + L;
     nsz[c + 1] = sz - L;
   }
@@ -1103,7 +1124,7 @@ __global__ void kd_relabel_kernel(int64_t n, const int* __restrict__ sbeg, const
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int sgm = segid[p];
-  segid[p] = cbase[sgm] + ((ssz[sgm] > TILE && (int)(p - sbeg[sgm]) >= ssplit[sgm]) ? 1 : 0);
+  segid[p] = cbase[sgm] + ((ssplit[sgm] < ssz[sgm] && (int)(p - sbeg[sgm]) >= ssplit[sgm]) ? 1 : 0);
 }
 
 // compact order -> padded positions: leaf k occupies tile k
@@ -1670,6 +1691,9 @@ struct nnm_dataset {
     stats.scan_ms += ms;
     stats.scans += 1;
     stats.tc_items += nfull;
+    if (getenv("NNM_DEBUG"))
+      fprintf(stderr, "[nnm] tc scan: %lld items, %.2f ms (%.0f ns/item)\n", (long long)nfull, ms,
+              1e6 * ms / (double)nfull);
     if (a.trace) {  // append the timeline of this launch (CTA 0, first 256 items)
       std::vector<long long> h(8 * 256 * 2 + 4);
       CUDA_TRY(cudaMemcpyAsync(h.data(), a.trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
@@ -1858,22 +1882,28 @@ struct nnm_dataset {
       DevBuf<unsigned long long> keys;
       keys.ensure(n);
       for (int lv = 0; lv < 64; ++lv) {
-        std::vector<int> hsz(nseg);
-        CUDA_TRY(cudaMemcpyAsync(hsz.data(), ssz.p, nseg * sizeof(int), cudaMemcpyDeviceToHost, st));
-        sync();
-        if (*std::max_element(hsz.begin(), hsz.end()) <= TILE) break;
+        // separated pieces may be cut off anywhere (and leaves split at a clear gap) in the
+        // first 32 levels; later levels only halve, so every segment ends <= TILE
+        const int allow_off = lv < 32 ? 1 : 0;
+        if (!allow_off) {
+          std::vector<int> hsz(nseg);
+          CUDA_TRY(cudaMemcpyAsync(hsz.data(), ssz.p, nseg * sizeof(int), cudaMemcpyDeviceToHost, st));
+          sync();
+          if (*std::max_element(hsz.begin(), hsz.end()) <= TILE) break;
+        }
         sdim.ensure(nseg);
         ssplit.ensure(nseg);
         nchild.ensure(nseg);
         cbase.ensure(nseg + 1);
-        kd_dim_kernel<<<nseg, 32, 0, st>>>(X64.p, d, order.p, sbeg.p, ssz.p, nseg, sdim.p); note_launch();
+        kd_dim_kernel<<<nseg, 32, 0, st>>>(X64.p, d, order.p, sbeg.p, ssz.p, nseg, allow_off, sdim.p); note_launch();
         kd_key_kernel<<<blocks_for(n), 256, 0, st>>>(X64.p, n, d, order.p, segid.p, sdim.p, keys.p); note_launch();
         thrust::stable_sort_by_key(thrust::cuda::par(talloc).on(st), keys.p, keys.p + n, order.p);
-        kd_splitpos_kernel<<<nseg, 32, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, ssplit.p); note_launch();
-        kd_children_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, ssz.p, nchild.p); note_launch();
+        kd_splitpos_kernel<<<nseg, 32, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, allow_off, ssplit.p); note_launch();
+        kd_children_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, ssz.p, ssplit.p, nchild.p); note_launch();
         thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), nchild.p, nchild.p + nseg, cbase.p, 0);
         int lastc = read1(nchild.p + (nseg - 1)), lastb = read1(cbase.p + (nseg - 1));
         const int nseg2 = lastb + lastc;
+        if (nseg2 == nseg) break;  // no segment split: every leaf is final
         nbeg.ensure(nseg2);
         nsz.ensure(nseg2);
         kd_newsegs_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, sbeg.p, ssz.p, ssplit.p, cbase.p, nbeg.p, nsz.p); note_launch();
