@@ -28,6 +28,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/nnm.h"
@@ -2070,7 +2071,8 @@ struct nnm_dataset {
     if (hi2 > lo2)
       scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, lo2, hi2, items2.p, false, tumax.p);
     if (rank == 0) pairs_covered += (double)n * (double)(n - 1) / 2.0;
-    if (getenv("NNM_DEBUG")) {
+    const char* dbg_env = getenv("NNM_DEBUG");
+    if (dbg_env && atoi(dbg_env) >= 2) {  // list statistics (expensive host copies)
       const int T = Tp;
       std::vector<double> rad(T), um(T);
       CUDA_TRY(cudaMemcpyAsync(rad.data(), tradius.p, T * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -2627,24 +2629,53 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       // ---------------- Boruvka: exact MST of the eligible graph, then replay
       ds->stats.path = NNM_PATH_BORUVKA;
       auto tp0 = std::chrono::steady_clock::now();
+      // the caller's output arrays are usually fresh pages: fault them in on host threads
+      // while the GPU rounds run, so the replay below writes to resident memory
+      std::vector<std::thread> prefault;
+      if (n > 4096) {
+        char* pm = reinterpret_cast<char*>(out_merges);
+        const size_t bm = (size_t)(n - 1) * sizeof(nnm_merge), half = bm / 2;
+        prefault.emplace_back([pm, half] { memset(pm, 0, half); });
+        prefault.emplace_back([pm, half, bm] { memset(pm + half, 0, bm - half); });
+        prefault.emplace_back([out_assign, n] { memset(out_assign, 0, (size_t)n * sizeof(int64_t)); });
+      }
+      struct Joiner {
+        std::vector<std::thread>& t;
+        ~Joiner() {
+          for (auto& th : t)
+            if (th.joinable()) th.join();
+        }
+      } joiner{prefault};
       ds->bv_begin(metric, cons->dmax);
       ds->sync();
       ds->stats.prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
       bool need = n > 1 && !(cons->kl1 > 0 && n <= cons->kl1);
       const char* pe = getenv("NNM_PRUNE");
       const bool prune = !(pe && pe[0] == '0');
+      const bool dbg_t = getenv("NNM_DEBUG") != nullptr;
       while (need && ds->bv_ncomp > 1) {
+        auto th0 = std::chrono::steady_clock::now();
         if (prune) {
           ds->pruned_scan(metric);
+          if (dbg_t) {
+            ds->sync();
+            fprintf(stderr, "[nnm] host: round scan %.2f ms\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
+          }
         } else {
           ds->scan(metric, ds->B1.p, ds->B2.p, true, INT_UNSET, INT_UNSET, ds->bv_thr_hi, 0,
                    ds->tile_pairs());
           ds->pairs_covered += (double)n * (double)(n - 1) / 2.0;
         }
+        auto th1 = std::chrono::steady_clock::now();
         int64_t added = ds->bv_finish_round(ds->B1.p, ds->B2.p);
+        if (dbg_t)
+          fprintf(stderr, "[nnm] host: round finish %.2f ms\n",
+                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th1).count());
         if (added == 0) break;
       }
       auto tr0 = std::chrono::steady_clock::now();
+      for (auto& th : prefault) th.join();
       ds->bv_end(cons->kl1, out_merges, out_n_merges, out_assign, out_rounds, out_stop);
       ds->stats.replay_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
     } else {
