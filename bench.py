@@ -7,8 +7,11 @@ single-linkage dendrogram (euclidean, no constraints).  One *step* = one full
 clustering run (all Boruvka rounds: fused FP32 screening scans, FP64 exact
 keys, hooking, sort + replay of the 1,999,999 merges).
 
-* ``value``   distance-pair evaluations per second over the step, inputs already
+* ``value``   seconds to the full dendrogram (lower is better) -- the BASELINE
+              headline ("2Mx25 NNM clustering time") -- with the inputs already
               resident in HBM (a DeviceDataset built before the timed region).
+              Distance-pair evaluations/s (evaluated pairs over the step) and the
+              pair space covered per second are in ``config``.
 * ``e2e``     the same metric through the public API (``engine.run``) with host
               buffers: float64 X uploaded, merge log + labels read back, every step.
 * ``roofline`` dominant kernel = the fused screening scan (tcgen05 TF32 tensor-core
@@ -18,7 +21,9 @@ keys, hooking, sort + replay of the 1,999,999 merges).
               bf16 figure); the FP32-roofline fraction the north star quotes (against
               the FFMA2 microbenchmark, nnm_measure_fp32_peak) is reported beside it.
 * ``cpu_baseline`` the C oracle (a port of the reference's round scan) on the
-              host cores, one top-P round on a bounded row sample.
+              host cores, one top-P round on a bounded row sample; its ``value`` is
+              the reference's job time EXTRAPOLATED from that sample as a lower
+              bound (round time at full n x ceil((n-1)/256) rounds), labelled so.
 
 ``--impl reference`` times the reference's CPU path (the oracle port: there is
 no compiled reference, the reference is pure Python + scipy) on the same
@@ -50,7 +55,9 @@ CONFIGS = {
     "c3": ("c3: 500k x 25, 1000 blobs, dmax=5.0", {"dmax": 5.0}),
     "c4": ("c4: 2M x 25, 4000 blobs (spread 1, seed 5), euclidean full dendrogram", {}),
 }
-METRIC = "NNM clustering distance-pair evaluations/s (BASELINE: 2Mx25 NNM clustering; pairs/s vs FP32 roofline)"
+METRIC = ("NNM single-linkage clustering time to the full dendrogram (s) (BASELINE: 2Mx25 NNM "
+          "clustering time; distance-pairs/s and the FP32 roofline are in config / roofline)")
+REF_P = 256  # the reference's default pairs_per_batch (engine.py:35)
 
 
 def _dist_env():
@@ -138,10 +145,19 @@ def cpu_baseline(X, seconds_target: float = 12.0) -> dict:
     m = int(min(X.shape[0], max(4000, (2 * rate * seconds_target) ** 0.5)))
     t = one(m)
     pairs = m * (m - 1) / 2
-    return {"value": pairs / t, "unit": "pairs/s", "cores": threads, "kind": "port",
-            "sample": f"one reference round (top-P=256 selection over all {pairs:.3g} pairs) on a "
-                      f"{m}-row strided sample of the {X.shape[0]}x{d} input; {t:.1f} s",
-            "seconds": t}
+    n = X.shape[0]
+    # EXTRAPOLATION (labelled): a reference round scans all n(n-1)/2 pairs at the sampled
+    # rate, and an unconstrained run merges at most P=256 pairs per round, so the full
+    # dendrogram needs >= ceil((n-1)/P) rounds -> a lower bound of the reference's job time
+    round_s = n * (n - 1) / 2 / (pairs / t)
+    rounds_lb = -(-(n - 1) // REF_P)
+    return {"value": rounds_lb * round_s, "unit": "s", "cores": threads, "kind": "port",
+            "sample": f"one reference round (top-P={REF_P} selection over all {pairs:.3g} pairs) on a "
+                      f"{m}-row strided sample of the {n}x{d} input; {t:.1f} s",
+            "extrapolation": f"value = LOWER BOUND extrapolated from the sample: round time at "
+                             f"n={n} (n(n-1)/2 pairs at the sampled rate) x ceil((n-1)/{REF_P}) rounds",
+            "pairs_per_s": pairs / t, "round_seconds_extrapolated": round_s,
+            "rounds_lower_bound": rounds_lb, "seconds": t}
 
 
 def run_reference(args) -> None:
@@ -159,15 +175,18 @@ def run_reference(args) -> None:
     v = statistics.median(s["value"] for s in samples)
     last = samples[-1]
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s",
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(s["seconds"] for s in samples),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": CONFIGS[args.config][0], "n": X.shape[0],
-                                        "d": X.shape[1]},
-        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": last["cores"], "kind": "port",
-                         "sample": last["sample"]},
-        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                                        "d": X.shape[1],
+                                        "pairs_per_s": statistics.median(s["pairs_per_s"] for s in samples),
+                                        "round_seconds_extrapolated": last["round_seconds_extrapolated"],
+                                        "rounds_lower_bound": last["rounds_lower_bound"]},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": last["cores"], "kind": "port",
+                         "sample": last["sample"], "extrapolation": last["extrapolation"]},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -294,7 +313,8 @@ def run_gpu(args) -> None:
         pe_e2e = pe
     e2e_ms_step = max_over_ranks(statistics.mean(e2e_ms))
     pe_e2e = sum_over_ranks(pe_e2e)
-    e2e = {"value": pe_e2e / (e2e_ms_step / 1e3), "unit": "pairs/s",
+    e2e = {"value": e2e_ms_step / 1e3, "unit": "s",
+           "pairs_evaluated_per_s": pe_e2e / (e2e_ms_step / 1e3),
            "h2d_bytes_per_step": int(X.nbytes) * world,
            "d2h_bytes_per_step": int((marr.nbytes + assign.nbytes) * world),
            "ms_per_step": e2e_ms_step,
@@ -356,12 +376,13 @@ def run_gpu(args) -> None:
     cfg = {"workload": desc, "n": n, "d": d, "metric": "euclidean", "pairs_per_step": pairs_step,
            "l2": "inputs larger than L2 (X32 %.0f MB + X64 %.0f MB > 126 MB)" % (n * d * 4 / 1e6, X.nbytes / 1e6),
            "seconds_to_dendrogram": ms_dev / 1e3, "boruvka_rounds": stats[-1]["boruvka_rounds"],
+           "pairs_evaluated_per_s": value,
            "pairs_covered_per_s": sum(s["pairs_covered"] for s in stats) / (ms_dev * args.steps / 1e3),
            "pairs_evaluated_fraction": pairs_eval / max(1.0, sum(s["pairs_covered"] for s in stats)),
            "merges": n - 1, "parallelism": f"tile-pair shards x{world}" if world > 1 else "1 GPU"}
     line = {
-        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": True,
+        "metric": METRIC, "value": ms_dev / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None,
         "dtype": ("tf32-tensor-screen+f64-exact" if tc_items > 0 else "fp32-screen+f64-exact"),
         "data": "synthetic (generate_synthetic, bit-identical to the reference generator)",
