@@ -741,7 +741,7 @@ __global__ void phase1_kernel(const float* __restrict__ c32, const float* __rest
                               const int2* __restrict__ trange, int T, int d, int2* __restrict__ out) {
   const int I0 = blockIdx.x * TR;
   const int nr = min(TR, T - I0);
-  __shared__ float ci[TR][192];
+  __shared__ __align__(16) float ci[TR][192];
   for (int t = threadIdx.x; t < TR * d; t += blockDim.x) {
     const int r = t / d, k = t % d;
     ci[r][k] = r < nr ? c32[(int64_t)k * T + I0 + r] : 0.f;
@@ -832,6 +832,130 @@ __global__ void phase1_kernel(const float* __restrict__ c32, const float* __rest
   }
 }
 
+// Phase 1, register form (d <= 32): one thread per row tile I and one of P1_CHUNKS
+// slices of the column tiles, I's centre in registers, column centres staged in shared
+// memory (broadcast reads); each thread keeps its slice's PK best (rank, J) in registers
+// (ties: smaller J), then phase1_merge_kernel takes the PK best of the slices.  Same
+// ranking as phase1_kernel; the selection is a heuristic seed set (any choice is sound).
+constexpr int P1_CHUNKS = 7;  // 138 x 7 blocks of 128: one wave on 148 SMs at 2M points
+constexpr int P1_ROWS = 128;
+constexpr int P1_JT = 64;
+
+template <int M, int D>
+__global__ void __launch_bounds__(P1_ROWS) phase1_reg_kernel(const float* __restrict__ c32,
+                                                             const float* __restrict__ r32,
+                                                             const int2* __restrict__ trange, int T,
+                                                             float* __restrict__ cand_l,
+                                                             int* __restrict__ cand_j) {
+  constexpr int d = D;  // compile-time: straight-line distance code
+  const int I = blockIdx.x * P1_ROWS + threadIdx.x;
+  const int chunk = blockIdx.y;
+  const int per = (T + P1_CHUNKS - 1) / P1_CHUNKS;
+  const int J0 = chunk * per, J1 = min(T, J0 + per);
+  __shared__ float sc[P1_JT][D + 1];
+  __shared__ float sr[P1_JT];
+  __shared__ int2 st[P1_JT];
+  const bool live = I < T;
+  float ci[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ci[k] = live ? __ldg(c32 + (int64_t)k * T + I) : 0.f;
+  const float rI = live ? r32[I] : 0.f;
+  const int2 trI = live ? trange[I] : make_int2(0, 1);
+  const bool singleI = trI.x == trI.y;
+  float bl[PK];
+  int bj[PK];
+#pragma unroll
+  for (int k = 0; k < PK; ++k) {
+    bl[k] = INFINITY;
+    bj[k] = -1;
+  }
+  for (int Jb = J0; Jb < J1; Jb += P1_JT) {
+    const int nj = min(P1_JT, J1 - Jb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < P1_JT * D; t += P1_ROWS) {
+      const int k = t / P1_JT, j = t % P1_JT;
+      sc[j][k] = j < nj ? __ldg(c32 + (int64_t)k * T + Jb + j) : 0.f;
+    }
+    if (threadIdx.x < P1_JT && threadIdx.x < nj) {
+      sr[threadIdx.x] = r32[Jb + threadIdx.x];
+      st[threadIdx.x] = trange[Jb + threadIdx.x];
+    }
+    __syncthreads();
+    if (!live) continue;
+    for (int j = 0; j < nj; ++j) {
+      const int J = Jb + j;
+      const int2 tJ = st[j];
+      if (singleI && tJ.x == tJ.y && tJ.x == trI.x) continue;  // same_single(I, J)
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float t = fabsf(ci[k] - sc[j][k]);
+        if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc = fmaf(t, t, acc);
+        else if (M == MANHATTAN) acc += t;
+        else acc = fmaxf(acc, t);
+      }
+      const float dc = (M == EUCLIDEAN || M == SQEUCLIDEAN) ? sqrtf(acc) : acc;
+      float v = (J == I) ? -INFINITY : dc - fminf(sr[j], rI);
+      if (!(v < bl[PK - 1])) continue;
+      int jj = J;
+#pragma unroll
+      for (int k = 0; k < PK; ++k) {
+        if (v < bl[k]) {
+          const float tv = bl[k];
+          const int tj = bj[k];
+          bl[k] = v;
+          bj[k] = jj;
+          v = tv;
+          jj = tj;
+        }
+      }
+    }
+  }
+  if (!live) return;
+  const int64_t o = ((int64_t)I * P1_CHUNKS + chunk) * PK;
+#pragma unroll
+  for (int k = 0; k < PK; ++k) {
+    cand_l[o + k] = bl[k];
+    cand_j[o + k] = bj[k];
+  }
+}
+
+__global__ void phase1_merge_kernel(const float* __restrict__ cand_l, const int* __restrict__ cand_j,
+                                    int T, int pk, int2* __restrict__ out) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= T) return;
+  const int64_t o = (int64_t)I * P1_CHUNKS * PK;
+  float bl[PK];
+  int bj[PK];
+#pragma unroll
+  for (int k = 0; k < PK; ++k) {
+    bl[k] = INFINITY;
+    bj[k] = -1;
+  }
+  // chunks hold ascending J ranges: visiting them in order keeps ties on the smaller J
+  for (int c = 0; c < P1_CHUNKS * PK; ++c) {
+    int jj = cand_j[o + c];
+    if (jj < 0) continue;
+    float v = cand_l[o + c];
+    if (!(v < bl[PK - 1])) continue;
+#pragma unroll
+    for (int k = 0; k < PK; ++k) {
+      if (v < bl[k]) {
+        const float tv = bl[k];
+        const int tj = bj[k];
+        bl[k] = v;
+        bj[k] = jj;
+        v = tv;
+        jj = tj;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < PK; ++k)
+    out[(int64_t)I * PK + k] = (k < pk && bj[k] >= 0) ? make_int2(min(I, bj[k]), max(I, bj[k]))
+                                                      : make_int2(-1, -1);
+}
+
 __device__ __forceinline__ int64_t tri_index(int T, int I, int J) {
   return (int64_t)I * T - (int64_t)I * (I - 1) / 2 + (J - I);
 }
@@ -885,7 +1009,7 @@ __global__ void enum_count_kernel(const float* __restrict__ c32, const float* __
                                   unsigned char* __restrict__ keep, int* __restrict__ counts) {
   const int I0 = blockIdx.x * TR;
   const int nr = min(TR, T - I0);
-  __shared__ float ci[TR][192];
+  __shared__ __align__(16) float ci[TR][192];
   for (int t = threadIdx.x; t < TR * d; t += blockDim.x) {
     const int r = t / d, k = t % d;
     ci[r][k] = r < nr ? c32[(int64_t)k * T + I0 + r] : 0.f;
@@ -1442,6 +1566,8 @@ struct nnm_dataset {
   DevBuf<double> tcenter, tradius, tumax;
   DevBuf<float> tc32, tcn32, tr32;  // fp32 SoA tile centres / norms / radii (tile passes)
   DevBuf<int2> items1, items2;
+  DevBuf<float> p1_l;  // phase-1 per-slice candidates (phase1_reg_kernel)
+  DevBuf<int> p1_j;
   // per tile pair (triangle index): fp32 bits of a lower bound of S over its cross-component
   // pairs, written by the tensor-core scan, read by the phase-2 enumeration (0: unknown)
   DevBuf<unsigned> tpmin;
@@ -1987,7 +2113,24 @@ struct nnm_dataset {
     const int64_t W = tile_pairs();
     // phase-1 seeds: PK nearest cross-capable tiles per tile
     items1.ensure((size_t)Tp * PK);
-    phase1_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
+    const char* p1e = getenv("NNM_P1REG");
+    if ((d == 25 || d == 8) && !(p1e && p1e[0] == '0')) {
+      p1_l.ensure((size_t)Tp * P1_CHUNKS * PK);
+      p1_j.ensure((size_t)Tp * P1_CHUNKS * PK);
+      const dim3 g((Tp + P1_ROWS - 1) / P1_ROWS, P1_CHUNKS);
+      if (d == 25)
+        phase1_reg_kernel<M, 25><<<g, P1_ROWS, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, p1_l.p, p1_j.p);
+      else
+        phase1_reg_kernel<M, 8><<<g, P1_ROWS, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, p1_l.p, p1_j.p);
+      note_launch();
+      const char* pke = getenv("NNM_PK");
+      // 4 seeds per tile: measured best on 2Mx25 (PK 8 -> 4: phase-1 scan -20%, the
+      // component bounds stay tight enough that phase 2 does not grow)
+      const int pk = pke ? std::max(1, std::min(PK, atoi(pke))) : 4;
+      phase1_merge_kernel<<<blocks_for(Tp), 256, 0, st>>>(p1_l.p, p1_j.p, Tp, pk, items1.p); note_launch();
+    } else {
+      phase1_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
+    }
     CUDA_TRY(cudaGetLastError());
     auto* k64 = reinterpret_cast<unsigned long long*>(items1.p);  // (I, J) -> J << 32 | I order
     // sort by (I, J): int2 memory is {x=I, y=J}; as u64 little-endian = J << 32 | I -> swap to key
