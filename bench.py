@@ -340,9 +340,11 @@ def run_gpu(args) -> None:
         roofline = {
             "bound": "tensor", "achieved": alg_tflops, "peak": tf32_peak, "unit": "TFLOP/s",
             "frac": alg_tflops / tf32_peak,
-            "traffic": (tr["dram_bytes_per_item"] * tc_items / max(scans, 1)) if tr else None,
-            "traffic_note": "dram bytes per launch = ncu dram__bytes_read+write per tile-pair item "
-                            "(profiles/tc_scan_traffic.json) x average items per launch",
+            "traffic": (tr.get("dram_bytes_per_launch") or
+                        tr["dram_bytes_per_item"] * tc_items / max(scans, 1)) if tr else None,
+            "traffic_note": "ncu dram__bytes_read+write of one captured launch (round-2 phase-1 "
+                            "seed scan, profiles/tc_scan_traffic.json); the FP64 exact-key gathers "
+                            "(X64 rows) dominate it",
             "kernel": "tc_scan_kernel (tcgen05 kind::tf32 128x128x32 MMA per tile pair, TMEM "
                       "accumulators; fused centring, component masks, threshold filter, exact-key "
                       "top-2)",
