@@ -1161,7 +1161,8 @@ __global__ void kd_key_kernel(const double* __restrict__ X64, int64_t n, int d,
 // split position of each segment (sorted by the split coordinate): the largest
 // gap in the middle half if it is a real gap (>= 10% of the extent), else the
 // multiple of 128 nearest the median.  Segments <= TILE are leaves.
-__global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
+constexpr int KD_SPLIT_THREADS = 256;
+__global__ void __launch_bounds__(KD_SPLIT_THREADS) kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
                                    const int* __restrict__ sbeg, const int* __restrict__ ssz,
                                    int nseg, int allow_off, int* __restrict__ ssplit) {
   const int sgm = blockIdx.x;
@@ -1204,7 +1205,27 @@ __global__ void kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
       bp2 = op;
     }
   }
+  // across the block's warps (a top-level segment holds all n points)
+  __shared__ float wg[KD_SPLIT_THREADS / 32], wg2[KD_SPLIT_THREADS / 32];
+  __shared__ int wp[KD_SPLIT_THREADS / 32], wp2[KD_SPLIT_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) {
+    wg[threadIdx.x >> 5] = bg;
+    wp[threadIdx.x >> 5] = bp;
+    wg2[threadIdx.x >> 5] = bg2;
+    wp2[threadIdx.x >> 5] = bp2;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      if (wg[w] > bg || (wg[w] == bg && wp[w] < bp)) {
+        bg = wg[w];
+        bp = wp[w];
+      }
+      if (wg2[w] > bg2 || (wg2[w] == bg2 && wp2[w] < bp2)) {
+        bg2 = wg2[w];
+        bp2 = wp2[w];
+      }
+    }
     const float ext = val(sz - 1) - val(0);
     if (sz <= TILE) {
       // a leaf that holds two separated groups (a piece of a neighbouring cluster) is
@@ -1740,6 +1761,18 @@ struct nnm_dataset {
   // operand image + bounds of the kd view for the tensor-core scan (once per dataset)
   void tc_prepare() {
     if (tc_ready) return;
+    auto tq0 = std::chrono::steady_clock::now();
+    struct Report {
+      nnm_dataset* ds;
+      std::chrono::steady_clock::time_point t0;
+      ~Report() {
+        if (getenv("NNM_DEBUG")) {
+          cudaStreamSynchronize(ds->st);
+          fprintf(stderr, "[nnm] host: tc operand image %.2f ms\n",
+                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        }
+      }
+    } report{this, tq0};
     tc_img.ensure((size_t)Tp * TC_TILE_FLOATS);
     tc_tnorm.ensure(np_);
     tc_eta.ensure(np_);
@@ -1923,12 +1956,25 @@ struct nnm_dataset {
   // ---------------------------------------------------------------- Boruvka
   void bv_begin(int metric, double dmax) {
     bv_metric = metric;
+    const bool dbg_t = getenv("NNM_DEBUG") != nullptr;
+    auto tb0 = std::chrono::steady_clock::now();
     use_boruvka_view();
+    if (dbg_t) {
+      sync();
+      fprintf(stderr, "[nnm] host: view (kd order) %.2f ms, %d tiles\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb0).count(), Tp);
+    }
     ensure_norms_p(metric);
     em = make_err_model(metric, d);
     bv_thr = INFINITY;
     bv_thr_hi = INFINITY;
+    auto tb1 = std::chrono::steady_clock::now();
     ensure_geometry(metric);
+    if (dbg_t) {
+      sync();
+      fprintf(stderr, "[nnm] host: norms + geometry %.2f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tb1).count());
+    }
     const char* de = getenv("NNM_DOT");
     dot_on = (metric == EUCLIDEAN || metric == SQEUCLIDEAN) && !(de && de[0] == '0') &&
              scan_use_ws(d);
@@ -2025,7 +2071,7 @@ struct nnm_dataset {
         kd_dim_kernel<<<nseg, 32, 0, st>>>(X64.p, d, order.p, sbeg.p, ssz.p, nseg, allow_off, sdim.p); note_launch();
         kd_key_kernel<<<blocks_for(n), 256, 0, st>>>(X64.p, n, d, order.p, segid.p, sdim.p, keys.p); note_launch();
         thrust::stable_sort_by_key(thrust::cuda::par(talloc).on(st), keys.p, keys.p + n, order.p);
-        kd_splitpos_kernel<<<nseg, 32, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, allow_off, ssplit.p); note_launch();
+        kd_splitpos_kernel<<<nseg, KD_SPLIT_THREADS, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, allow_off, ssplit.p); note_launch();
         kd_children_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, ssz.p, ssplit.p, nchild.p); note_launch();
         thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), nchild.p, nchild.p + nseg, cbase.p, 0);
         int lastc = read1(nchild.p + (nseg - 1)), lastb = read1(cbase.p + (nseg - 1));
