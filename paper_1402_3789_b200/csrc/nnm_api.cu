@@ -1552,6 +1552,17 @@ struct nnm_dataset {
   DevBuf<Edge> edges;
   DevBuf<ReplayEdge> replay;
   PinnedBuf<ReplayEdge> host_replay;
+  // host replay scratch (reused across runs; faulted in during the GPU rounds by nnm_run)
+  std::vector<int32_t> rp_par, rp_sz, rp_keep, rp_drop, rp_size;
+  void replay_host_buffers() {
+    if ((int64_t)rp_par.size() < n) {
+      rp_par.resize(n);
+      rp_sz.resize(n);
+      rp_keep.resize(n);
+      rp_drop.resize(n);
+      rp_size.resize(n);
+    }
+  }
   DevBuf<int2> pairs;
   DevBuf<double> pair_d;
   DevBuf<int> flag;
@@ -2389,9 +2400,19 @@ struct nnm_dataset {
     }
     auto tq0 = std::chrono::steady_clock::now();
     // union-find replay (model.py:109-187): union keeps the smaller root (int32 forest,
-    // path halving; roots are always the minimum index of their cluster)
-    std::vector<int32_t> par(n), sz(n, 1);
-    for (int64_t i = 0; i < n; ++i) par[i] = (int32_t)i;
+    // path halving; roots are always the minimum index of their cluster).  The sequential
+    // loop writes 12 B per merge (kept root, dropped root, new size); the 56-byte merge
+    // records are then assembled by several threads.
+    replay_host_buffers();
+    std::vector<int32_t>& par = rp_par;
+    std::vector<int32_t>& sz = rp_sz;
+    for (int64_t i = 0; i < n; ++i) {
+      par[i] = (int32_t)i;
+      sz[i] = 1;
+    }
+    int32_t* RK = rp_keep.data();
+    int32_t* RD = rp_drop.data();
+    int32_t* RS = rp_size.data();
     auto find = [&](int32_t x) {
       while (par[x] != x) {
         par[x] = par[par[x]];
@@ -2420,21 +2441,47 @@ struct nnm_dataset {
         par[drop] = keep;
         sz[keep] += sz[drop];
         --count;
-        nnm_merge& m = out[nm++];
-        m.round = e.round;
-        m.root_a = keep;
-        m.root_b = drop;
-        m.dist = e.dist;  // reported units (metrics.py:86-90)
-        m.new_size = sz[keep];
-        m.point_a = e.a;
-        m.point_b = e.b;
+        RK[nm] = keep;
+        RD[nm] = drop;
+        RS[nm] = sz[keep];
+        ++nm;
         reason = stop_of(count);
         if (reason) break;
       }
       if (!reason) reason = NNM_STOP_NO_ELIGIBLE;
     }
     auto tq1 = std::chrono::steady_clock::now();
-    for (int64_t i = 0; i < n; ++i) assign[i] = find((int32_t)i);
+    // merge records and labels in parallel (read-only finds: the forest is final)
+    const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, std::min<int64_t>(
+                       (int64_t)std::thread::hardware_concurrency(), (n >> 16) + 1)));
+    auto work = [&](int t) {
+      const int64_t m0 = nm * t / nt, m1 = nm * (t + 1) / nt;
+      for (int64_t k = m0; k < m1; ++k) {
+        const ReplayEdge& e = h[k];
+        nnm_merge& m = out[k];
+        m.round = e.round;
+        m.root_a = RK[k];
+        m.root_b = RD[k];
+        m.dist = e.dist;  // reported units (metrics.py:86-90)
+        m.new_size = RS[k];
+        m.point_a = e.a;
+        m.point_b = e.b;
+      }
+      const int64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
+      for (int64_t i = i0; i < i1; ++i) {
+        int32_t x = (int32_t)i;
+        while (par[x] != x) x = par[x];
+        assign[i] = x;
+      }
+    };
+    if (nt == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> pool;
+      for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+      work(0);
+      for (auto& th : pool) th.join();
+    }
     *n_merges = nm;
     *rounds = (n > 1 && stop_of(n) == 0) ? bv_round : 0;
     *stop = reason;
@@ -2827,6 +2874,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
         prefault.emplace_back([pm, half] { memset(pm, 0, half); });
         prefault.emplace_back([pm, half, bm] { memset(pm + half, 0, bm - half); });
         prefault.emplace_back([out_assign, n] { memset(out_assign, 0, (size_t)n * sizeof(int64_t)); });
+        prefault.emplace_back([ds] { ds->replay_host_buffers(); });
       }
       struct Joiner {
         std::vector<std::thread>& t;
