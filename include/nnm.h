@@ -148,6 +148,13 @@ int nnm_bv_scan(nnm_dataset *ds, int64_t w_begin, int64_t w_end, uint64_t *B1_de
  * list in full (so all ranks derive identical component bounds with no exchange)
  * and its contiguous 1/world share of the phase-2 items; keys land in (B1, B2).
  * world == 1 is the whole single-GPU pruned scan. */
+/* Tile-pair bound cache of the staged Boruvka run (valid after nnm_bv_begin): device
+ * pointer and count of the per-tile-pair uint32 lower bounds (fp32 bits, 0 = unknown;
+ * NULL / 0 when off: non-TC metric, or NNM_TPCACHE=0).  synced = 1 declares that the
+ * caller all-reduces the array with MAX (as int32 or uint32: the bits of non-negative
+ * floats) across ranks after every nnm_bv_scan_pruned; only then do multi-rank pruned
+ * scans use it (every rank must derive the same phase-2 list). */
+int nnm_bv_cache(nnm_dataset *ds, int32_t synced, void **out_ptr, int64_t *out_count);
 int nnm_bv_scan_pruned(nnm_dataset *ds, int32_t rank, int32_t world, uint64_t *B1_dev,
                        uint64_t *B2_dev);
 /* B2 contribution for the global second-best: B2c[i] = (B1loc[i] == B1glob[i]) ? B2loc[i] : B1loc[i] */

@@ -36,7 +36,7 @@ EXPORTED = (
     "nnm_dataset_create_device", "nnm_dataset_destroy", "nnm_top_p", "nnm_run",
     "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_scan_pruned", "nnm_bv_second", "nnm_bv_finish_round",
     "nnm_bv_end", "nnm_measure_fp32_peak", "nnm_tc_probe", "nnm_csv_load", "nnm_csv_fetch",
-    "nnm_csv_free", "nnm_first_nonfinite",
+    "nnm_csv_free", "nnm_first_nonfinite", "nnm_bv_cache",
 )
 
 
@@ -113,6 +113,7 @@ def load():
         lib.nnm_csv_fetch.argtypes = [vp, vp, vp, vp]
         lib.nnm_csv_free.argtypes = [vp]
         lib.nnm_first_nonfinite.argtypes = [vp, i64, i32, P(i64)]
+        lib.nnm_bv_cache.argtypes = [vp, i32, P(vp), P(i64)]
         lib.nnm_bv_second.argtypes = [vp, vp, vp, vp, vp]
         lib.nnm_bv_finish_round.argtypes = [vp, vp, vp, P(i64)]
         lib.nnm_bv_end.argtypes = [vp, i64, vp, P(i64), vp, P(i64), P(i32), P(Stats)]

@@ -1604,7 +1604,8 @@ struct nnm_dataset {
   // pairs, written by the tensor-core scan, read by the phase-2 enumeration (0: unknown)
   DevBuf<unsigned> tpmin;
   bool tpmin_on = false;   // allocated and reset for this run
-  bool tpmin_use = false;  // this scan may read / write it (single-rank scans only)
+  bool tpmin_use = false;  // this scan may read / write it
+  bool tpmin_sync = false; // multi-rank caller all-reduces (MAX) the cache after every scan
   DevBuf<unsigned> pbits;
   DevBuf<unsigned char> pkeep;
   DevBuf<int> pcount;
@@ -2019,6 +2020,7 @@ struct nnm_dataset {
     // tile-pair bound cache (TC scan only; 4 B per tile pair: 0.58 GB at 2M points)
     const char* ce = getenv("NNM_TPCACHE");
     tpmin_use = false;
+    tpmin_sync = false;
     tpmin_on = tc_on && !(ce && ce[0] == '0') && tile_pairs() * 4 <= ((int64_t)4 << 30);
     if (tpmin_on) {
       tpmin.ensure(tile_pairs());
@@ -2244,9 +2246,10 @@ struct nnm_dataset {
   void pruned_scan_shard(int metric, unsigned long long* b1, unsigned long long* b2, int rank,
                          int world) {
     ensure_geometry(metric);
-    // every rank must derive the same phase-2 list without an exchange: the cache holds
-    // rank-local bounds, so only a single-rank scan reads or writes it
-    tpmin_use = tpmin_on && world == 1;
+    // every rank must derive the same phase-2 list: the cache holds rank-local bounds of
+    // the phase-2 items, so a multi-rank scan uses it only when the caller all-reduces it
+    // (MAX) after every scan (nnm_bv_cache); the phase-1 writes are identical on all ranks
+    tpmin_use = tpmin_on && (world == 1 || tpmin_sync);
     tile_range.ensure(Tp);
     tile_range_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, Tp, tile_range.p); note_launch();
     int64_t n1 = 0, n2 = 0;
@@ -3090,6 +3093,16 @@ __global__ void second_kernel(int n, const unsigned long long* b1l, const unsign
 }  // namespace nnm
 
 extern "C" {
+int nnm_bv_cache(nnm_dataset* ds, int32_t synced, void** out_ptr, int64_t* out_count) {
+  return guarded([&] {
+    if (!ds || !out_ptr || !out_count) invalid("null argument");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    ds->tpmin_sync = ds->tpmin_on && synced != 0;
+    *out_ptr = ds->tpmin_on ? (void*)ds->tpmin.p : nullptr;
+    *out_count = ds->tpmin_on ? ds->tile_pairs() : 0;
+  });
+}
+
 int nnm_bv_scan_pruned(nnm_dataset* ds, int32_t rank, int32_t world, uint64_t* B1_dev,
                        uint64_t* B2_dev) {
   return guarded([&] {

@@ -30,6 +30,14 @@ __all__ = ["shard_range", "combine_second", "run_boruvka_distributed",
            "run_boruvka_distributed_handle"]
 
 
+class _DeviceArray:
+    """A library-owned device buffer seen through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous equal-count share of [0, total) for `rank`."""
     lo = total * rank // world
@@ -80,6 +88,14 @@ def run_boruvka_distributed_handle(dd, *, metric="euclidean", dmax=None, kl1=Non
                                    np.nan if dmax is None else float(dmax), ctypes.byref(tp),
                                    ctypes.byref(rows)))
     n = dd.n
+    # tile-pair bound cache (TC metric): kept identical on every rank by an all-reduce(MAX)
+    # after each pruned scan, so the ranks keep deriving the same phase-2 lists
+    cptr, ccount = ctypes.c_void_p(), ctypes.c_int64()
+    _native.check(lib.nnm_bv_cache(dd.handle, 1 if (world > 1 and pruned) else 0,
+                                   ctypes.byref(cptr), ctypes.byref(ccount)))
+    cache = None
+    if world > 1 and pruned and cptr.value and ccount.value > 0:
+        cache = torch.as_tensor(_DeviceArray(cptr.value, ccount.value, "<i4"), device="cuda")
     lo, hi = shard_range(tp.value, rank, world)
     b1 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
     b2 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
@@ -94,6 +110,8 @@ def run_boruvka_distributed_handle(dd, *, metric="euclidean", dmax=None, kl1=Non
         else:
             _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
         torch.cuda.synchronize()
+        if cache is not None:
+            dist.all_reduce(cache, op=dist.ReduceOp.MAX, group=group)
         g1.copy_(b1)
         dist.all_reduce(g1, op=dist.ReduceOp.MIN, group=group)
         _native.check(lib.nnm_bv_second(dd.handle, b1.data_ptr(), b2.data_ptr(), g1.data_ptr(),
