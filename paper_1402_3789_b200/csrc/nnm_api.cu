@@ -1014,6 +1014,17 @@ __global__ void enum_count_kernel(const float* __restrict__ c32, const float* __
     const int r = t / d, k = t % d;
     ci[r][k] = r < nr ? c32[(int64_t)k * T + I0 + r] : 0.f;
   }
+  // per-row-tile constants (read once per block, broadcast from shared memory)
+  __shared__ float rcn[TR], rr[TR];
+  __shared__ double ru[TR];
+  __shared__ int2 rtr[TR];
+  if (threadIdx.x < TR) {
+    const int r = threadIdx.x;
+    rcn[r] = r < nr ? cn[I0 + r] : 0.f;
+    rr[r] = r < nr ? r32[I0 + r] : 0.f;
+    ru[r] = r < nr ? umax[I0 + r] : 0.0;
+    rtr[r] = r < nr ? trange[I0 + r] : make_int2(0, 1);
+  }
   __syncthreads();
   int c[TR];
 #pragma unroll
@@ -1023,18 +1034,22 @@ __global__ void enum_count_kernel(const float* __restrict__ c32, const float* __
     cdist32_rows<M>(c32, T, ci, J, d, dc);
     const double uJ = umax[J];
     const float cnJ = cn[J], rJ = r32[J];
+    const int2 tJ = trange[J];
 #pragma unroll
     for (int r = 0; r < TR; ++r) {
       const int I = I0 + r;
       if (r >= nr || J < I) continue;
       const int64_t w = tri_index(T, I, J);
-      bool k = !((bits[w >> 5] >> (w & 31)) & 1u) && !same_single(trange, I, J);
+      const int2 tI = rtr[r];
+      bool k = !((bits[w >> 5] >> (w & 31)) & 1u) &&
+               !(tI.x == tI.y && tJ.x == tJ.y && tI.x == tJ.x);  // same_single(I, J)
       // kept iff the rigorous lower bound of the tile pair can reach either component
-      // bound (a kept superset costs work, never exactness)
+      // bound (a kept superset costs work, never exactness); the cached bound (a scanned
+      // pair's) is read only when the geometric one passes
       if (k && J != I) {
-        double lb = tile_lb32<M>(dc[r], cn[I], cnJ, r32[I], rJ, d);
-        if (tpmin) lb = fmax(lb, (double)__uint_as_float(tpmin[w]));  // scanned before: its bound
-        k = lb <= fmax(umax[I], uJ);
+        const double ub = fmax(ru[r], uJ);
+        k = tile_lb32<M>(dc[r], rcn[r], cnJ, rr[r], rJ, d) <= ub;
+        if (k && tpmin) k = (double)__uint_as_float(tpmin[w]) <= ub;
       }
       keep[w] = k;
       c[r] += k;
