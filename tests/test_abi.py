@@ -61,3 +61,27 @@ def test_validation_errors_before_device():
         nnm.RunConfig(pairs_per_batch=0)
     with pytest.raises(nnm.ValidationError):
         nnm.Dataset(values=np.array([[np.nan]]))
+
+
+def test_dataset_finite_check_host_only():
+    """nnm_first_nonfinite is host code (no GPU): the Dataset check of model.py:29-76 with the
+    reference's message, for NaN / +-inf anywhere, at sizes that use several threads."""
+    if not os.path.exists(LIB):
+        pytest.skip("libnnm.so not built")
+    from paper_1402_3789_b200 import Dataset, ValidationError
+    from paper_1402_3789_b200 import _native
+
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(300_001, 7))
+    assert _native.first_nonfinite(np.ascontiguousarray(X)) == -1
+    Dataset(values=X)
+    for flat, bad in ((0, np.nan), (5, np.inf), (X.size // 2 + 3, -np.inf), (X.size - 1, np.nan)):
+        Y = X.copy()
+        Y.reshape(-1)[flat] = bad
+        assert _native.first_nonfinite(Y) == flat
+        with pytest.raises(ValidationError, match=f"non-finite feature value in row {flat // 7 + 1}$"):
+            Dataset(values=Y)
+    Z = X.copy()
+    Z[10, 2] = np.nan
+    Z[200_000, 1] = np.inf  # the first one wins
+    assert _native.first_nonfinite(Z) == 10 * 7 + 2
