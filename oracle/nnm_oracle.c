@@ -140,6 +140,8 @@ typedef struct {
   int has_thr;
   double thr;
   int64_t kl2, kl3; /* <0: unset */
+  const double *XT; /* d x ldt transposed copy (zero padded), built once per call */
+  int64_t ldt;
 } scan_ctx_t;
 
 /* pairgen.py:169-187: roots differ, dist <= thr, sizes <= kl2, sa+sb <= kl3 */
@@ -161,41 +163,62 @@ typedef struct {
   int64_t *next_row; /* shared work counter */
   pthread_mutex_t *mu;
   heap_t heap;
-  int64_t evaluated;
 } worker_t;
 
 #define ROW_CHUNK 16
 #define COL_BLOCK 256
+#define RB 4  /* rows per register block */
+#define CV 8  /* doubles per vector */
 
-/* Distances of row x to the columns of a transposed block yT[d][cb]: every
- * pair still accumulates left to right over k (SIMD lanes are different
- * pairs), so values stay bit-identical to orc_internal_distance. */
+typedef double v8d __attribute__((vector_size(64)));
+typedef long long v8l __attribute__((vector_size(64)));
+
+/* Distances of RB rows x[r] to the columns of a transposed block yT[d][COL_BLOCK]
+ * (zero padded past cb).  Register-blocked: RB x 2 vectors of accumulators, every
+ * yT load is shared by RB rows.  Each pair still accumulates strictly left to right
+ * over k with separate IEEE sub / mul / add (SIMD lanes are different pairs; this
+ * file is compiled with -ffp-contract=off), so every value stays bit-identical to
+ * orc_internal_distance (scipy cdist order). */
 __attribute__((target_clones("avx512f", "avx2", "default")))
-static void block_dist(int metric, const double *x, const double *yT, int d, int cb, double *acc) {
-  for (int b = 0; b < cb; b++) acc[b] = 0.0;
-  if (metric == ORC_EUCLIDEAN || metric == ORC_SQEUCLIDEAN) {
+static void block_dist(int metric, const double *const *x, const double *yT, int64_t ldt, int d,
+                       int cb, double (*acc)[COL_BLOCK]) {
+  const v8l absmask = {~(1LL << 63), ~(1LL << 63), ~(1LL << 63), ~(1LL << 63),
+                       ~(1LL << 63), ~(1LL << 63), ~(1LL << 63), ~(1LL << 63)};
+  for (int c0 = 0; c0 < cb; c0 += 2 * CV) {
+    v8d a0[RB], a1[RB];
+    for (int r = 0; r < RB; r++) {
+      a0[r] = (v8d){0, 0, 0, 0, 0, 0, 0, 0};
+      a1[r] = a0[r];
+    }
     for (int k = 0; k < d; k++) {
-      const double xk = x[k];
-      const double *y = yT + (size_t)k * cb;
-      for (int b = 0; b < cb; b++) {
-        double t = xk - y[b];
-        acc[b] = acc[b] + t * t;
+      v8d y0, y1;
+      memcpy(&y0, yT + (size_t)k * ldt + c0, sizeof(v8d));
+      memcpy(&y1, yT + (size_t)k * ldt + c0 + CV, sizeof(v8d));
+      for (int r = 0; r < RB; r++) {
+        const double xs = x[r][k];
+        const v8d xv = {xs, xs, xs, xs, xs, xs, xs, xs};
+        v8d t0 = xv - y0, t1 = xv - y1;
+        if (metric == ORC_EUCLIDEAN || metric == ORC_SQEUCLIDEAN) {
+          v8d s0 = t0 * t0, s1 = t1 * t1;
+          a0[r] = a0[r] + s0;
+          a1[r] = a1[r] + s1;
+        } else {
+          t0 = (v8d)((v8l)t0 & absmask);
+          t1 = (v8d)((v8l)t1 & absmask);
+          if (metric == ORC_MANHATTAN) {
+            a0[r] = a0[r] + t0;
+            a1[r] = a1[r] + t1;
+          } else { /* chebyshev: acc = (t > acc) ? t : acc */
+            v8l m0 = t0 > a0[r], m1 = t1 > a1[r];
+            a0[r] = (v8d)(((v8l)t0 & m0) | ((v8l)a0[r] & ~m0));
+            a1[r] = (v8d)(((v8l)t1 & m1) | ((v8l)a1[r] & ~m1));
+          }
+        }
       }
     }
-  } else if (metric == ORC_MANHATTAN) {
-    for (int k = 0; k < d; k++) {
-      const double xk = x[k];
-      const double *y = yT + (size_t)k * cb;
-      for (int b = 0; b < cb; b++) acc[b] = acc[b] + fabs(xk - y[b]);
-    }
-  } else {
-    for (int k = 0; k < d; k++) {
-      const double xk = x[k];
-      const double *y = yT + (size_t)k * cb;
-      for (int b = 0; b < cb; b++) {
-        double t = fabs(xk - y[b]);
-        acc[b] = (t > acc[b]) ? t : acc[b];
-      }
+    for (int r = 0; r < RB; r++) {
+      memcpy(&acc[r][c0], &a0[r], sizeof(v8d));
+      memcpy(&acc[r][c0 + CV], &a1[r], sizeof(v8d));
     }
   }
 }
@@ -205,8 +228,7 @@ static void *topp_worker(void *arg) {
   const scan_ctx_t *c = w->ctx;
   const int64_t n = c->n;
   const int d = c->d;
-  double *yT = (double *)malloc((size_t)d * COL_BLOCK * sizeof(double));
-  double acc[COL_BLOCK];
+  double(*acc)[COL_BLOCK] = (double(*)[COL_BLOCK])malloc(sizeof(double) * RB * COL_BLOCK);
   for (;;) {
     int64_t r0;
     pthread_mutex_lock(w->mu);
@@ -217,23 +239,32 @@ static void *topp_worker(void *arg) {
     int64_t r1 = r0 + ROW_CHUNK < n ? r0 + ROW_CHUNK : n;
     for (int64_t b0 = r0 + 1; b0 < n; b0 += COL_BLOCK) {
       const int cb = (int)(n - b0 < COL_BLOCK ? n - b0 : COL_BLOCK);
-      for (int j = 0; j < cb; j++)
-        for (int k = 0; k < d; k++) yT[(size_t)k * cb + j] = c->X[(b0 + j) * d + k];
-      for (int64_t a = r0; a < r1; a++) {
-        if (a + 1 >= b0 + cb) continue;
-        block_dist(c->metric, c->X + a * d, yT, d, cb, acc);
-        for (int j = 0; j < cb; j++) {
-          const int64_t b = b0 + j;
-          if (b <= a || !pre_eligible(c, a, b)) continue;
-          const double dist = acc[j];
-          w->evaluated++;
-          if (c->has_thr && dist > c->thr) continue; /* pairgen.py:197-198 */
-          heap_offer(&w->heap, dist, a, b);
+      const double *yT = c->XT + b0; /* lanes past cb read the zero padding, never used */
+      for (int64_t ag = r0; ag < r1; ag += RB) {
+        if (ag + 1 >= b0 + cb) continue;
+        const double *xr[RB];
+        for (int r = 0; r < RB; r++) xr[r] = c->X + (ag + r < r1 ? ag + r : ag) * d;
+        block_dist(c->metric, xr, yT, c->ldt, d, cb, acc);
+        for (int r = 0; r < RB && ag + r < r1; r++) {
+          const int64_t a = ag + r;
+          /* a pair whose distance exceeds the threshold (pairgen.py:197-198) or the
+           * largest key of a full heap cannot be selected: skip it before the
+           * eligibility lookups (the selection itself is unchanged) */
+          double lim = c->has_thr ? c->thr : INFINITY;
+          if (w->heap.len == w->heap.cap && w->heap.v[0].d < lim) lim = w->heap.v[0].d;
+          for (int j = (b0 > a ? 0 : (int)(a + 1 - b0)); j < cb; j++) {
+            const double dist = acc[r][j];
+            if (dist > lim) continue;
+            const int64_t b = b0 + j;
+            if (!pre_eligible(c, a, b)) continue;
+            heap_offer(&w->heap, dist, a, b);
+            if (w->heap.len == w->heap.cap && w->heap.v[0].d < lim) lim = w->heap.v[0].d;
+          }
         }
       }
     }
   }
-  free(yT);
+  free(acc);
   return NULL;
 }
 
@@ -242,7 +273,11 @@ int64_t orc_top_p(const double *X, int64_t n, int d, int metric, const int64_t *
                   int nthreads, double *out_d, int64_t *out_a, int64_t *out_b) {
   if (P < 1 || n < 1 || d < 1) return -1; /* pairgen.py:256-257 */
   if (nthreads < 1) nthreads = 1;
-  scan_ctx_t c = {X, n, d, metric, roots, sizes, !isnan(thr), thr, kl2, kl3};
+  const int64_t ldt = n + 2 * COL_BLOCK;
+  double *XT = (double *)calloc((size_t)d * ldt, sizeof(double));
+  for (int64_t i = 0; i < n; i++)
+    for (int k = 0; k < d; k++) XT[(size_t)k * ldt + i] = X[i * d + k];
+  scan_ctx_t c = {X, n, d, metric, roots, sizes, !isnan(thr), thr, kl2, kl3, XT, ldt};
   int64_t npairs = n * (n - 1) / 2;
   int64_t cap = P < npairs ? P : npairs;
   if (cap < 1) cap = 1;
@@ -284,6 +319,7 @@ int64_t orc_top_p(const double *X, int64_t n, int d, int metric, const int64_t *
   free(all);
   free(ws);
   free(th);
+  free(XT);
   return len;
 }
 
