@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define NNM_ABI_VERSION 1
+#define NNM_ABI_VERSION 2
 
 enum {
   NNM_OK = 0,
@@ -93,6 +93,8 @@ typedef struct {
                               (each a 128x128x32 kind::tf32 MMA); 0 on the FP32 path */
   int64_t round_rescans;   /* round path: rounds whose reused row bounds were too loose, so
                               the full scan ran (rounds - 1 - round_rescans were reused) */
+  int64_t replay_gpu_merges; /* merges replayed on the GPU (nnm_replay.cu); the rest, if
+                                any, by the sequential host loop */
 } nnm_stats;
 
 int nnm_abi_version(void);

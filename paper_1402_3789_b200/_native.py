@@ -26,6 +26,7 @@ NNM_E_UNSUPPORTED = -3
 NNM_E_NOMEM = -4
 NNM_E_CAPACITY = -5
 
+ABI_VERSION = 2  # include/nnm.h NNM_ABI_VERSION
 FLAG_ROUNDS = 1
 PATH_NAMES = {0: "none", 1: "boruvka", 2: "rounds"}
 STOP_NAMES = {1: "kl1-reached", 2: "no-eligible-pairs", 3: "single-cluster"}
@@ -52,7 +53,8 @@ class Stats(ctypes.Structure):
                 ("exact_evals", ctypes.c_int64), ("boruvka_rounds", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_int64), ("pairs_covered", ctypes.c_double),
                 ("prep_ms", ctypes.c_double), ("replay_ms", ctypes.c_double),
-                ("tc_items", ctypes.c_int64), ("round_rescans", ctypes.c_int64)]
+                ("tc_items", ctypes.c_int64), ("round_rescans", ctypes.c_int64),
+                ("replay_gpu_merges", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -95,6 +97,9 @@ def load():
         P = ctypes.POINTER
         i64, i32, dbl, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
         lib.nnm_abi_version.restype = ctypes.c_int
+        if lib.nnm_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {lib.nnm_abi_version()}, this package needs "
+                              f"{ABI_VERSION}: rebuild it with __graft_entry__.build()")
         lib.nnm_last_error.restype = ctypes.c_char_p
         lib.nnm_device_count.argtypes = [P(i32)]
         lib.nnm_dataset_create.argtypes = [vp, i64, i32, i32, P(vp)]

@@ -421,11 +421,6 @@ struct EdgeLess {
   }
 };
 
-struct ReplayEdge {  // host-side replay record (sorted order)
-  double dist;        // reported distance (sqrt for euclidean)
-  int a, b, round, pad;
-};
-
 __global__ void replay_edges_kernel(const Edge* __restrict__ e, int64_t ne, int sqrt_dist,
                                     ReplayEdge* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1539,7 +1534,8 @@ struct nnm_dataset {
   int T = 0;
   int sms = 148;
   cudaStream_t st = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  cudaStream_t st2 = nullptr;  // side stream for device-to-host copies that overlap kernels
 
   DevBuf<double> X64;
   DevBuf<float> X32;
@@ -1567,6 +1563,13 @@ struct nnm_dataset {
   DevBuf<Edge> edges;
   DevBuf<ReplayEdge> replay;
   PinnedBuf<ReplayEdge> host_replay;
+  PinnedBuf<int32_t> h_rk, h_rd, h_rs, h_as;
+  DevBuf<int> r_par, r_sz, r_lab, r_head, r_ea, r_eb, r_nxt, r_comp, r_ctl, r_rk, r_rd, r_rs;
+  cudaGraphExec_t rp_exec = nullptr;  // captured replay chunk sequence (see bv_end)
+  int64_t rp_m = -1, rp_n = -1, rp_nch = -1;
+  int rp_lmax = -1;
+  const void* rp_e = nullptr;
+  ReplayState rp_state{};
   // host replay scratch (reused across runs; faulted in during the GPU rounds by nnm_run)
   std::vector<int32_t> rp_par, rp_sz, rp_keep, rp_drop, rp_size;
   void replay_host_buffers() {
@@ -1647,6 +1650,12 @@ struct nnm_dataset {
     talloc.release();
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
+    if (rp_exec) cudaGraphExecDestroy(rp_exec);
+    if (st2) {
+      cudaStreamSynchronize(st2);
+      cudaStreamDestroy(st2);
+    }
   }
 
   void sync() { CUDA_TRY(cudaStreamSynchronize(st)); }
@@ -2400,10 +2409,22 @@ struct nnm_dataset {
   }
 
   // sort edges by (d, a, b) and replay them through a min-root union-find
+  // (model.py:109-187, engine.py:90-143): the kept root is the smaller index, roots are
+  // always the minimum index of their cluster.  The replay runs on the GPU
+  // (nnm_replay.cu: rank chunks, component-parallel); a chunk whose longest component
+  // exceeds lmax -- and everything after it -- is finished by the sequential host loop.
   void bv_end(int64_t kl1, nnm_merge* out, int64_t* n_merges, int64_t* assign, int64_t* rounds,
               int32_t* stop) {
-    unsigned long long ne = read1(counters.p);
-    // sorted edges, reported distances computed on the device, copied into pinned memory
+    const unsigned long long ne = read1(counters.p);
+    auto stop_of = [&](int64_t c) -> int {
+      if (c == 1) return NNM_STOP_SINGLE_CLUSTER;
+      if (kl1 >= 0 && c <= kl1) return NNM_STOP_KL1;
+      return 0;
+    };
+    // the reference stops at the first count that is a stop reason (engine.py:139-142)
+    const int64_t floor_count = (kl1 >= 0) ? std::max<int64_t>(kl1, 1) : 1;
+    const int64_t m = stop_of(n) ? 0 : std::min<int64_t>((int64_t)ne, std::max<int64_t>(n - floor_count, 0));
+    auto tq0 = std::chrono::steady_clock::now();
     ReplayEdge* h = nullptr;
     if (ne > 0) {
       thrust::sort(thrust::cuda::par(talloc).on(st), edges.p, edges.p + ne, EdgeLess());
@@ -2413,42 +2434,164 @@ struct nnm_dataset {
                                                                    replay.p); note_launch();
       CUDA_TRY(cudaGetLastError());
       h = host_replay.ensure(ne);
-      CUDA_TRY(cudaMemcpyAsync(h, replay.p, ne * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st));
-      sync();
+      // the 24-byte records travel on the side stream while the replay kernels run
+      CUDA_TRY(cudaEventRecord(ev2, st));
+      CUDA_TRY(cudaStreamWaitEvent(st2, ev2, 0));
+      CUDA_TRY(cudaMemcpyAsync(h, replay.p, ne * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st2));
     }
-    auto tq0 = std::chrono::steady_clock::now();
-    // union-find replay (model.py:109-187): union keeps the smaller root (int32 forest,
-    // path halving; roots are always the minimum index of their cluster).  The sequential
-    // loop writes 12 B per merge (kept root, dropped root, new size); the 56-byte merge
-    // records are then assembled by several threads.
-    replay_host_buffers();
+    const bool dbg = getenv("NNM_DEBUG") != nullptr;
+    auto lap = [&](const char* what) {
+      if (!dbg) return;
+      sync();
+      fprintf(stderr, "[nnm]   replay %s at %.2f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count());
+    };
+    lap("sorted");
+    int32_t* RK = h_rk.ensure(std::max<int64_t>(m, 1));
+    int32_t* RD = h_rd.ensure(std::max<int64_t>(m, 1));
+    int32_t* RS = h_rs.ensure(std::max<int64_t>(m, 1));
+    int32_t* AS = nullptr;  // labels from the GPU (nullptr: host finds)
+    int64_t host_from = 0;  // first merge replayed on the host
+    const char* ge = getenv("NNM_GPU_REPLAY");
+    const bool gpu = m >= 32768 && !(ge && ge[0] == '0');
     std::vector<int32_t>& par = rp_par;
     std::vector<int32_t>& sz = rp_sz;
-    for (int64_t i = 0; i < n; ++i) {
-      par[i] = (int32_t)i;
-      sz[i] = 1;
-    }
-    int32_t* RK = rp_keep.data();
-    int32_t* RD = rp_drop.data();
-    int32_t* RS = rp_size.data();
-    auto find = [&](int32_t x) {
-      while (par[x] != x) {
-        par[x] = par[par[x]];
-        x = par[x];
+    replay_host_buffers();
+    auto tq1 = tq0;
+    if (gpu) {
+      const char* ce = getenv("NNM_REPLAY_CHUNKS");
+      const char* le = getenv("NNM_REPLAY_LMAX");
+      const int64_t nchunks = std::max<int64_t>(1, ce ? atoll(ce) : 24);
+      const int lmax = std::min(REPLAY_LMAX, le ? std::max(1, atoi(le)) : REPLAY_LMAX);
+      // chunk plan: uniform chunks over the first 7/8 of the ranks, then each chunk half
+      // of what is left (>= 1024 edges) -- the top of a blob dendrogram (the edges that
+      // join the blobs) is one component, so the host tail starts as late as possible
+      std::vector<std::pair<int64_t, int>> plan;
+      {
+        const int64_t C = std::max<int64_t>(4096, (m + nchunks - 1) / nchunks);
+        const int64_t head_end = m - m / 8;
+        int64_t lo = 0;
+        while (lo < head_end) {
+          const int64_t c = std::min<int64_t>(C, head_end - lo);
+          plan.emplace_back(lo, (int)c);
+          lo += c;
+        }
+        while (lo < m) {
+          const int64_t c = std::min<int64_t>(m - lo, std::max<int64_t>(1024, (m - lo) / 2));
+          plan.emplace_back(lo, (int)c);
+          lo += c;
+        }
       }
-      return x;
-    };
-    int64_t count = n, nm = 0;
-    auto stop_of = [&](int64_t c) -> int {
-      if (c == 1) return NNM_STOP_SINGLE_CLUSTER;
-      if (kl1 >= 0 && c <= kl1) return NNM_STOP_KL1;
-      return 0;
-    };
-    int reason = stop_of(count);
-    if (!reason) {
-      constexpr unsigned long long kAhead = 16;  // prefetch the forest entries of later merges
-      for (unsigned long long t = 0; t < ne; ++t) {
-        if (t + kAhead < ne) {
+      int cmax_chunk = 0;
+      for (auto& pc : plan) cmax_chunk = std::max(cmax_chunk, pc.second);
+      r_par.ensure(n);
+      r_sz.ensure(n);
+      r_lab.ensure(n);
+      r_head.ensure(n);
+      r_ea.ensure(cmax_chunk);
+      r_eb.ensure(cmax_chunk);
+      r_nxt.ensure(cmax_chunk);
+      r_comp.ensure(cmax_chunk);
+      r_ctl.ensure(4);
+      r_rk.ensure(m);
+      r_rd.ensure(m);
+      r_rs.ensure(m);
+      ReplayState rs{r_par.p, r_sz.p, r_lab.p, r_head.p, r_ea.p, r_eb.p, r_nxt.p, r_comp.p,
+                     r_ctl.p, r_rk.p, r_rd.p, r_rs.p};
+      const int64_t nch = (int64_t)plan.size();
+      const char* gre = getenv("NNM_REPLAY_GRAPH");
+      const bool use_graph = !dbg && !(gre && gre[0] == '0');
+      if (use_graph) {
+        // fixed launch topology for this (state, m, plan): captured once, replayed after
+        const bool same = rp_exec && rp_m == m && rp_n == n && rp_lmax == lmax &&
+                          rp_e == replay.p && rp_nch == nch &&
+                          memcmp(&rp_state, &rs, sizeof(rs)) == 0;
+        if (!same) {
+          if (rp_exec) cudaGraphExecDestroy(rp_exec);
+          rp_exec = nullptr;
+          cudaGraph_t gr = nullptr;
+          CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          cudaError_t ce2 = replay_init(n, rs, st);
+          for (auto& pc : plan)
+            if (ce2 == cudaSuccess) ce2 = replay_chunk(replay.p, pc.first, pc.second, lmax, rs, st);
+          const cudaError_t ce3 = cudaStreamEndCapture(st, &gr);
+          CUDA_TRY(ce2);
+          CUDA_TRY(ce3);
+          const cudaError_t ce4 = cudaGraphInstantiate(&rp_exec, gr, 0);
+          cudaGraphDestroy(gr);
+          CUDA_TRY(ce4);
+          rp_m = m;
+          rp_n = n;
+          rp_lmax = lmax;
+          rp_e = replay.p;
+          rp_nch = nch;
+          rp_state = rs;
+        }
+        CUDA_TRY(cudaGraphLaunch(rp_exec, st));
+      } else {
+        CUDA_TRY(replay_init(n, rs, st));
+        DevBuf<int> cmax;
+        if (dbg) {
+          cmax.ensure(nch);
+          CUDA_TRY(cudaMemsetAsync(cmax.p, 0, nch * sizeof(int), st));
+        }
+        for (int64_t c = 0; c < nch; ++c)
+          CUDA_TRY(replay_chunk(replay.p, plan[c].first, plan[c].second, lmax, rs, st,
+                                dbg ? cmax.p + c : nullptr));
+        if (dbg) {
+          std::vector<int> hc(nch);
+          CUDA_TRY(cudaMemcpyAsync(hc.data(), cmax.p, nch * sizeof(int), cudaMemcpyDeviceToHost, st));
+          sync();
+          fprintf(stderr, "[nnm]   replay chunks (size:longest component):");
+          for (int64_t c = 0; c < nch; ++c) fprintf(stderr, " %d:%d", plan[c].second, hc[c]);
+          fprintf(stderr, "\n");
+        }
+      }
+      g_launches.fetch_add(1 + 5 * nch, std::memory_order_relaxed);
+      lap("chunks");
+      int ctl[4];
+      CUDA_TRY(cudaMemcpyAsync(ctl, r_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, st));
+      sync();
+      if (ctl[3]) throw NnmError{NNM_E_CUDA, "boruvka produced a cycle (internal error)"};
+      host_from = ctl[1] < 0 ? m : ctl[1];
+      stats.replay_gpu_merges = host_from;
+      if (host_from > 0) {
+        CUDA_TRY(cudaMemcpyAsync(RK, r_rk.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(RD, r_rd.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(RS, r_rs.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      }
+      if (host_from == m) {
+        AS = h_as.ensure(n);
+        CUDA_TRY(replay_assign(n, rs, r_lab.p, st));
+        note_launch();
+        CUDA_TRY(cudaMemcpyAsync(AS, r_lab.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      } else {  // host finishes: the forest as the GPU left it (state at chunk start)
+        CUDA_TRY(cudaMemcpyAsync(par.data(), r_par.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(sz.data(), r_sz.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      }
+      sync();
+      if (dbg)
+        fprintf(stderr, "[nnm] gpu replay: %lld of %lld merges, %lld chunks, longest component %d\n",
+                (long long)host_from, (long long)m, (long long)nch, ctl[2]);
+    } else {
+      for (int64_t i = 0; i < n; ++i) {
+        par[i] = (int32_t)i;
+        sz[i] = 1;
+      }
+    }
+    CUDA_TRY(cudaStreamSynchronize(st2));
+    tq1 = std::chrono::steady_clock::now();
+    if (host_from < m) {
+      auto find = [&](int32_t x) {
+        while (par[x] != x) {
+          par[x] = par[par[x]];
+          x = par[x];
+        }
+        return x;
+      };
+      constexpr int64_t kAhead = 16;  // prefetch the forest entries of later merges
+      for (int64_t t = host_from; t < m; ++t) {
+        if (t + kAhead < m) {
           __builtin_prefetch(&par[h[t + kAhead].a], 1);
           __builtin_prefetch(&par[h[t + kAhead].b], 1);
         }
@@ -2458,17 +2601,14 @@ struct nnm_dataset {
         const int32_t keep = std::min(ra, rb), drop = std::max(ra, rb);
         par[drop] = keep;
         sz[keep] += sz[drop];
-        --count;
-        RK[nm] = keep;
-        RD[nm] = drop;
-        RS[nm] = sz[keep];
-        ++nm;
-        reason = stop_of(count);
-        if (reason) break;
+        RK[t] = keep;
+        RD[t] = drop;
+        RS[t] = sz[keep];
       }
-      if (!reason) reason = NNM_STOP_NO_ELIGIBLE;
     }
-    auto tq1 = std::chrono::steady_clock::now();
+    const int64_t nm = m;
+    const int reason = (n > 0 && stop_of(n - nm)) ? stop_of(n - nm) : NNM_STOP_NO_ELIGIBLE;
+    auto tq2 = std::chrono::steady_clock::now();
     // merge records and labels in parallel (read-only finds: the forest is final)
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, std::min<int64_t>(
                        (int64_t)std::thread::hardware_concurrency(), (n >> 16) + 1)));
@@ -2476,20 +2616,24 @@ struct nnm_dataset {
       const int64_t m0 = nm * t / nt, m1 = nm * (t + 1) / nt;
       for (int64_t k = m0; k < m1; ++k) {
         const ReplayEdge& e = h[k];
-        nnm_merge& m = out[k];
-        m.round = e.round;
-        m.root_a = RK[k];
-        m.root_b = RD[k];
-        m.dist = e.dist;  // reported units (metrics.py:86-90)
-        m.new_size = RS[k];
-        m.point_a = e.a;
-        m.point_b = e.b;
+        nnm_merge& mg = out[k];
+        mg.round = e.round;
+        mg.root_a = RK[k];
+        mg.root_b = RD[k];
+        mg.dist = e.dist;  // reported units (metrics.py:86-90)
+        mg.new_size = RS[k];
+        mg.point_a = e.a;
+        mg.point_b = e.b;
       }
       const int64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
-      for (int64_t i = i0; i < i1; ++i) {
-        int32_t x = (int32_t)i;
-        while (par[x] != x) x = par[x];
-        assign[i] = x;
+      if (AS) {
+        for (int64_t i = i0; i < i1; ++i) assign[i] = AS[i];
+      } else {
+        for (int64_t i = i0; i < i1; ++i) {
+          int32_t x = (int32_t)i;
+          while (par[x] != x) x = par[x];
+          assign[i] = x;
+        }
       }
     };
     if (nt == 1) {
@@ -2504,9 +2648,10 @@ struct nnm_dataset {
     *rounds = (n > 1 && stop_of(n) == 0) ? bv_round : 0;
     *stop = reason;
     if (getenv("NNM_DEBUG"))
-      fprintf(stderr, "[nnm] replay: loop %.1f ms, assign %.1f ms\n",
+      fprintf(stderr, "[nnm] replay: device %.1f ms, host loop %.1f ms, records %.1f ms\n",
               std::chrono::duration<double, std::milli>(tq1 - tq0).count(),
-              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq1).count());
+              std::chrono::duration<double, std::milli>(tq2 - tq1).count(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq2).count());
   }
 
   // ---------------------------------------------------------------- top-P
@@ -2694,6 +2839,8 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
     t_alloc_stream = ds->st;
     CUDA_TRY(cudaEventCreate(&ds->ev0));
     CUDA_TRY(cudaEventCreate(&ds->ev1));
+    CUDA_TRY(cudaEventCreateWithFlags(&ds->ev2, cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithFlags(&ds->st2, cudaStreamNonBlocking));
     if ((size_t)ds->d * TILE * 2 * sizeof(float) + 8192 > 200 * 1024)
       throw NnmError{NNM_E_UNSUPPORTED, "d too large for the shared-memory tile (d <= 190)"};
     auto tc0 = std::chrono::steady_clock::now();

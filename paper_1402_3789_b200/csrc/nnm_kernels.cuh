@@ -51,6 +51,29 @@ struct CollectArgs {
   unsigned long long cap;
 };
 
+struct ReplayEdge {  // sorted MST edge for the merge replay
+  double dist;        // reported distance (sqrt for euclidean)
+  int a, b, round, pad;
+};
+
+// GPU merge replay (nnm_replay.cu): forest state + one chunk's scratch
+constexpr int REPLAY_LMAX = 128;  // longest component replayed on the GPU
+struct ReplayState {
+  int* par;   // [n] union-find over points (roots = minimum index, model.py:148-160)
+  int* sz;    // [n] cluster size at each root
+  int* lab;   // [n] scratch labels for the per-chunk components
+  int* head;  // [n] per-component list heads
+  int *ea, *eb;       // [chunk] roots of the edge ends at chunk start
+  int *nxt, *comp;    // [chunk] list links, component label per edge
+  int* ctl;  // [0] stop flag, [1] first edge the host must replay (-1: none), [2] max
+             // component length seen, [3] cycle detected (internal error)
+  int *rk, *rd, *rs;  // [m] kept root, dropped root, new size per merge
+};
+cudaError_t replay_init(int64_t n, const ReplayState& s, cudaStream_t st);
+cudaError_t replay_chunk(const ReplayEdge* e, int64_t lo, int cnt, int lmax, const ReplayState& s,
+                         cudaStream_t st, int* chunk_max = nullptr);
+cudaError_t replay_assign(int64_t n, const ReplayState& s, int* out, cudaStream_t st);
+
 size_t scan_smem_bytes(int d);
 size_t collect_smem_bytes(int d);
 int scan_occupancy(int metric, int d);
