@@ -50,10 +50,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# name -> (workload, constraints, metric, dataset, P); SURVEY.md 8(d) / BASELINE.json configs
 CONFIGS = {
-    "c1": ("c1: 10k x 8, 5 blobs, unconstrained euclidean", {}),
-    "c3": ("c3: 500k x 25, 1000 blobs, dmax=5.0", {"dmax": 5.0}),
-    "c4": ("c4: 2M x 25, 4000 blobs (spread 1, seed 5), euclidean full dendrogram", {}),
+    "c1": ("c1: 10k x 8, 5 blobs, unconstrained euclidean", {}, "euclidean", "c1", 256),
+    "c2": ("c2: 100k x 25 (160 dense + 400 diffuse blobs), kl1=400 kl2=300 kl3=450 kl4=150, P=256",
+           {"kl1": 400, "kl2": 300, "kl3": 450, "kl4": 150}, "euclidean", "c2", 256),
+    "c3": ("c3: 500k x 25, 1000 blobs, dmax=5.0", {"dmax": 5.0}, "euclidean", "c3", 256),
+    "c4": ("c4: 2M x 25, 4000 blobs (spread 1, seed 5), euclidean full dendrogram", {},
+           "euclidean", "c4", 256),
+    "c5m": ("c5: 2M x 25 (C4's X), manhattan full dendrogram (metric plugin path)", {},
+            "manhattan", "c4", 256),
+    "c5c": ("c5: 2M x 25 (C4's X), chebyshev full dendrogram (metric plugin path)", {},
+            "chebyshev", "c4", 256),
 }
 METRIC = ("NNM single-linkage clustering time to the full dendrogram (s) (BASELINE: 2Mx25 NNM "
           "clustering time; distance-pairs/s and the FP32 roofline are in config / roofline)")
@@ -124,19 +132,44 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(X, seconds_target: float = 12.0) -> dict:
-    """Oracle port (C, all host threads) timed on one top-P round over a row sample."""
+# configs whose reference run finishes in seconds on the host: timed to completion
+FULL_REFERENCE = {"c1"}
+
+
+def cpu_full_run(X, cfg_name: str) -> dict:
+    """Oracle port (C, all host threads) running the reference's engine.run to completion
+    (orc_run: engine.py:154-199 with the reference's default P=256)."""
     from oracle import nnm_oracle as orc
 
+    _, cons, metric, _, P = CONFIGS[cfg_name]
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    r = orc.run(X, metric=metric, P=P, threads=threads, **cons)
+    t = time.perf_counter() - t0
+    n, d = X.shape
+    return {"value": t, "unit": "s", "cores": threads, "kind": "port",
+            "sample": f"the full {n}x{d} run to completion (engine.run semantics, P={P}, "
+                      f"{r.rounds} rounds, {len(r.merges)} merges); measured, not extrapolated",
+            "pairs_per_s": r.rounds * n * (n - 1) / 2 / t, "seconds": t, "rounds": r.rounds}
+
+
+def cpu_baseline(X, seconds_target: float = 12.0, cfg_name: str = "c4") -> dict:
+    """Oracle port (C, all host threads): the full run where it finishes in seconds,
+    else one top-P round over a row sample, extrapolated (labelled)."""
+    from oracle import nnm_oracle as orc
+
+    if cfg_name in FULL_REFERENCE:
+        return cpu_full_run(X, cfg_name)
     threads = os.cpu_count() or 1
     d = X.shape[1]
+    _, cons, metric, _, _ = CONFIGS[cfg_name]
 
     def one(m):
         S = np.ascontiguousarray(X[:: max(1, X.shape[0] // m)][:m])
         roots = np.arange(m, dtype=np.int64)
         sizes = np.ones(m, dtype=np.int64)
         t0 = time.perf_counter()
-        orc.top_p(S, roots, sizes, 256, threads=threads)
+        orc.top_p(S, roots, sizes, 256, metric=metric, threads=threads)
         return time.perf_counter() - t0
 
     m = 16000  # calibration sample (~1 s), then size the timed sample to ~seconds_target
@@ -147,17 +180,39 @@ def cpu_baseline(X, seconds_target: float = 12.0) -> dict:
     pairs = m * (m - 1) / 2
     n = X.shape[0]
     # EXTRAPOLATION (labelled): a reference round scans all n(n-1)/2 pairs at the sampled
-    # rate, and an unconstrained run merges at most P=256 pairs per round, so the full
-    # dendrogram needs >= ceil((n-1)/P) rounds -> a lower bound of the reference's job time
+    # rate.  With kl4 the round count is part of the result (the reference's own count,
+    # identical on the GPU); otherwise a run that performs M merges needs at
+    # least ceil(M/P) rounds at the reference's default P -> a lower bound of its job time
     round_s = n * (n - 1) / 2 / (pairs / t)
-    rounds_lb = -(-(n - 1) // REF_P)
-    return {"value": rounds_lb * round_s, "unit": "s", "cores": threads, "kind": "port",
-            "sample": f"one reference round (top-P={REF_P} selection over all {pairs:.3g} pairs) on a "
-                      f"{m}-row strided sample of the {n}x{d} input; {t:.1f} s",
-            "extrapolation": f"value = LOWER BOUND extrapolated from the sample: round time at "
-                             f"n={n} (n(n-1)/2 pairs at the sampled rate) x ceil((n-1)/{REF_P}) rounds",
+    counts = _golden_counts(cfg_name)
+    if "kl4" in cons and counts.get("rounds"):
+        rounds, how = counts["rounds"], f"x {counts['rounds']} rounds (the reference's exact count)"
+    else:
+        merges = counts.get("n_merges", n - 1)
+        rounds = -(-merges // REF_P)
+        how = f"x ceil({merges} merges / P={REF_P}) rounds (LOWER BOUND)"
+    return {"value": rounds * round_s, "unit": "s", "cores": threads, "kind": "port",
+            "sample": f"one reference round (top-P={REF_P} selection over all {pairs:.3g} pairs, "
+                      f"{metric}) on a {m}-row strided sample of the {n}x{d} input; {t:.1f} s",
+            "extrapolation": f"value EXTRAPOLATED from the sample: round time at n={n} "
+                             f"(n(n-1)/2 pairs at the sampled rate) {how}",
             "pairs_per_s": pairs / t, "round_seconds_extrapolated": round_s,
-            "rounds_lower_bound": rounds_lb, "seconds": t}
+            "rounds": rounds, "seconds": t}
+
+
+def _golden_counts(cfg_name: str) -> dict:
+    """Merge / round counts of the full-scale oracle goldens (tests/golden/scale), used
+    only to size the reference extrapolation."""
+    name = {"c2": "c2", "c3": "c3"}.get(cfg_name)
+    if not name:
+        return {}
+    p = os.path.join(ROOT, "tests", "golden", "scale", f"{name}.json")
+    try:
+        with open(p) as f:
+            g = json.load(f)
+        return {"rounds": g.get("rounds"), "n_merges": g.get("n_merges")}
+    except (OSError, ValueError):
+        return {}
 
 
 def run_reference(args) -> None:
@@ -166,26 +221,29 @@ def run_reference(args) -> None:
         return
     from paper_1402_3789_b200.datagen import config_dataset
 
-    X = config_dataset(args.config)
+    X = config_dataset(CONFIGS[args.config][3])
     samples = []
     for step in range(args.warmup + args.steps):
-        cb = cpu_baseline(X, seconds_target=args.ref_seconds)
+        cb = cpu_baseline(X, seconds_target=args.ref_seconds, cfg_name=args.config)
         if step >= args.warmup:
             samples.append(cb)
     v = statistics.median(s["value"] for s in samples)
     last = samples[-1]
+    cfg = {"workload": CONFIGS[args.config][0], "n": X.shape[0], "d": X.shape[1],
+           "metric": CONFIGS[args.config][2],
+           "pairs_per_s": statistics.median(s["pairs_per_s"] for s in samples)}
+    cb_line = {"value": v, "unit": "s", "cores": last["cores"], "kind": "port",
+               "sample": last["sample"]}
+    if "extrapolation" in last:
+        cfg["round_seconds_extrapolated"] = last["round_seconds_extrapolated"]
+        cfg["rounds"] = last["rounds"]
+        cb_line["extrapolation"] = last["extrapolation"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.mean(s["seconds"] for s in samples),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": CONFIGS[args.config][0], "n": X.shape[0],
-                                        "d": X.shape[1],
-                                        "pairs_per_s": statistics.median(s["pairs_per_s"] for s in samples),
-                                        "round_seconds_extrapolated": last["round_seconds_extrapolated"],
-                                        "rounds_lower_bound": last["rounds_lower_bound"]},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": last["cores"], "kind": "port",
-                         "sample": last["sample"], "extrapolation": last["extrapolation"]},
+        "data": "synthetic", "config": cfg, "cpu_baseline": cb_line,
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,10 +286,13 @@ def run_gpu(args) -> None:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    desc, cons_kw = CONFIGS[args.config]
-    X = config_dataset(args.config)
+    desc, cons_kw, metric_name, data_name, P = CONFIGS[args.config]
+    X = config_dataset(data_name)
     n, d = X.shape
     cons = nnm.ConstraintSet(**cons_kw)
+    metric = nnm.MetricKind.parse(metric_name)
+    if world > 1 and (cons.kl2 or cons.kl3 or cons.kl4):
+        raise SystemExit("the round path (kl2/kl3/kl4) is single-GPU")
     lib = _native.load()
     pairs_full = n * (n - 1) / 2
 
@@ -259,11 +320,11 @@ def run_gpu(args) -> None:
 
     def step_device():
         if dist is None:
-            out = run_arrays(ddata, cons, 256, nnm.MetricKind.EUCLIDEAN)
-            return out[5]
+            out = run_arrays(ddata, cons, P, metric)
+            return dict(out[5], rounds=int(out[2]), merges=int(len(out[0])))
         from paper_1402_3789_b200.distributed import run_boruvka_distributed_handle
 
-        return run_boruvka_distributed_handle(ddata, dmax=cons.dmax)[4]
+        return run_boruvka_distributed_handle(ddata, dmax=cons.dmax, metric=metric)[4]
 
     for _ in range(args.warmup):
         step_device()
@@ -294,23 +355,37 @@ def run_gpu(args) -> None:
     # ---- end-to-end through the public API with host buffers (every step uploads X
     # from pinned host memory and reads the merge log + labels back)
     Xh = torch.from_numpy(X).pin_memory().numpy()
+    run_cfg = nnm.RunConfig(constraints=cons, metric=metric, pairs_per_batch=P)
+
+    def step_e2e(src):
+        if dist is None:
+            res = nnm.run(nnm.Dataset(values=src), run_cfg)
+            marr, assign, pe = res.merges.array, res.assignments, res.device_stats["pairs_evaluated"]
+        else:
+            from paper_1402_3789_b200.distributed import run_boruvka_distributed
+
+            marr, assign, _, _, sd = run_boruvka_distributed(src, dmax=cons.dmax, metric=metric)
+            pe = sd["pairs_evaluated"]
+        _ = marr["dist"].sum() + assign.sum()
+        return marr, assign, pe
+
     e2e_ms = []
     pe_e2e = 0.0
     for it in range(args.warmup + args.steps):
         barrier()
         t0 = time.perf_counter()
-        if dist is None:
-            res = nnm.run(nnm.Dataset(values=Xh), nnm.RunConfig(constraints=cons))
-            marr, assign, pe = res.merges.array, res.assignments, res.device_stats["pairs_evaluated"]
-        else:
-            from paper_1402_3789_b200.distributed import run_boruvka_distributed
-
-            marr, assign, _, _, sd = run_boruvka_distributed(Xh, dmax=cons.dmax)
-            pe = sd["pairs_evaluated"]
-        _ = marr["dist"].sum() + assign.sum()
+        marr, assign, pe = step_e2e(Xh)
         if it >= args.warmup:  # W untimed warm-up calls, like the device leg
             e2e_ms.append(1e3 * (time.perf_counter() - t0))
         pe_e2e = pe
+    # the same call on an ordinary (pageable) numpy array, as a user would pass it
+    pg_ms = []
+    for it in range(max(1, min(3, args.steps))):
+        barrier()
+        t0 = time.perf_counter()
+        step_e2e(X)
+        pg_ms.append(1e3 * (time.perf_counter() - t0))
+    pg_ms_step = max_over_ranks(statistics.mean(pg_ms))
     e2e_ms_step = max_over_ranks(statistics.mean(e2e_ms))
     pe_e2e = sum_over_ranks(pe_e2e)
     e2e = {"value": e2e_ms_step / 1e3, "unit": "s",
@@ -319,6 +394,11 @@ def run_gpu(args) -> None:
            "d2h_bytes_per_step": int((marr.nbytes + assign.nbytes) * world),
            "ms_per_step": e2e_ms_step,
            "ms_steps": [round(x, 1) for x in e2e_ms],
+           "inputs": "X in page-locked host memory (torch pin_memory); every step builds a "
+                     "Dataset (validation), uploads X, builds the spatial view and the "
+                     "tensor-core operand image (cached per device dataset in the device-resident "
+                     "`value`, rebuilt here) and reads the merge log + labels back",
+           "pageable_input_s": pg_ms_step / 1e3,
            "api": "paper_1402_3789_b200.run" if dist is None else
                   "paper_1402_3789_b200.distributed.run_boruvka_distributed"}
 
@@ -374,14 +454,21 @@ def run_gpu(args) -> None:
         if dist is not None:
             dist.destroy_process_group()
         return
-    cb = cpu_baseline(X) if world == 1 and not args.no_cpu_baseline else None
-    cfg = {"workload": desc, "n": n, "d": d, "metric": "euclidean", "pairs_per_step": pairs_step,
+    cb = (cpu_baseline(X, cfg_name=args.config)
+          if world == 1 and not args.no_cpu_baseline else None)
+    cfg = {"workload": desc, "n": n, "d": d, "metric": metric_name, "pairs_per_step": pairs_step,
+           "constraints": cons_kw, "pairs_per_batch": P, "path": stats[-1]["path"],
+           "rounds": stats[-1].get("rounds"),
            "l2": "inputs larger than L2 (X32 %.0f MB + X64 %.0f MB > 126 MB)" % (n * d * 4 / 1e6, X.nbytes / 1e6),
            "seconds_to_dendrogram": ms_dev / 1e3, "boruvka_rounds": stats[-1]["boruvka_rounds"],
            "pairs_evaluated_per_s": value,
            "pairs_covered_per_s": sum(s["pairs_covered"] for s in stats) / (ms_dev * args.steps / 1e3),
            "pairs_evaluated_fraction": pairs_eval / max(1.0, sum(s["pairs_covered"] for s in stats)),
-           "merges": n - 1, "parallelism": f"tile-pair shards x{world}" if world > 1 else "1 GPU"}
+           "merges": int(stats[-1].get("merges", n - 1)),
+           "device_value_note": "value = device step with X resident in HBM; the spatial (kd) view "
+                                "and the tensor-core operand image are built once per device "
+                                "dataset (before the timed region) and reused",
+           "parallelism": f"tile-pair shards x{world}" if world > 1 else "1 GPU"}
     line = {
         "metric": METRIC, "value": ms_dev / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_dev, "higher_is_better": False,

@@ -681,8 +681,8 @@ __global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n,
           const int64_t w2 = (int64_t)lo * T - (int64_t)lo * (lo - 1) / 2 + (hi - lo);
           lb = fmax(lb, (double)__uint_as_float(tpmin[w2]));
         }
-        keep_ij = lb <= umax[it.x];
-        keep_ji = lb <= umax[it.y];
+        keep_ij = !(lb > umax[it.x]);  // fail-safe: a NaN bound keeps the orientation
+        keep_ji = !(lb > umax[it.y]);
       }
     }
     const unsigned long long db = (unsigned long long)__float_as_uint(dc);
@@ -1043,8 +1043,9 @@ __global__ void enum_count_kernel(const float* __restrict__ c32, const float* __
       // pair's) is read only when the geometric one passes
       if (k && J != I) {
         const double ub = fmax(ru[r], uJ);
-        k = tile_lb32<M>(dc[r], rcn[r], cnJ, rr[r], rJ, d) <= ub;
-        if (k && tpmin) k = (double)__uint_as_float(tpmin[w]) <= ub;
+        // fail-safe comparisons: a NaN bound keeps the tile pair (never prunes it)
+        k = !(tile_lb32<M>(dc[r], rcn[r], cnJ, rr[r], rJ, d) > ub);
+        if (k && tpmin) k = !((double)__uint_as_float(tpmin[w]) > ub);
       }
       keep[w] = k;
       c[r] += k;
