@@ -1456,6 +1456,11 @@ __global__ void tile_range_kernel(const int* __restrict__ comp, int64_t n, int T
   }
 }
 
+__global__ void fill_u32_kernel(unsigned* p, int64_t n, unsigned v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
 __global__ void fill_u64_kernel(unsigned long long* p, int64_t n, unsigned long long v) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -1622,6 +1627,10 @@ struct nnm_dataset {
   // per tile pair (triangle index): fp32 bits of a lower bound of S over its cross-component
   // pairs, written by the tensor-core scan, read by the phase-2 enumeration (0: unknown)
   DevBuf<unsigned> tpmin;
+  // component caps (TC scan): bound pass over the phase-1 items, then capped exact scans
+  DevBuf<unsigned> ucap;
+  bool tc_cap_on = false;      // caps in use for this round's scans
+  bool tc_bound_first = false; // the next tc_scan runs the bound pass first (phase 1)
   bool tpmin_on = false;   // allocated and reset for this run
   bool tpmin_use = false;  // this scan may read / write it
   bool tpmin_sync = false; // multi-rank caller all-reduces (MAX) the cache after every scan
@@ -1663,6 +1672,11 @@ struct nnm_dataset {
 
   // key arrays start at NONE_KEY (INT64_MAX: signed and unsigned min agree, so
   // NCCL / gloo int64 all-reduce(MIN) combines them correctly)
+  void fill_u32(unsigned* p, int64_t cnt, unsigned v) {
+    fill_u32_kernel<<<blocks_for(cnt), 256, 0, st>>>(p, cnt, v); note_launch();
+    CUDA_TRY(cudaGetLastError());
+  }
+
   void fill_none(unsigned long long* p, int64_t cnt) {
     fill_u64_kernel<<<blocks_for(cnt), 256, 0, st>>>(p, cnt, NONE_KEY); note_launch();
     CUDA_TRY(cudaGetLastError());
@@ -1867,6 +1881,8 @@ struct nnm_dataset {
     a.B2 = b2;
     a.dump = nullptr;
     a.tpmin = tpmin_use ? tpmin.p : nullptr;
+    a.ucap = tc_cap_on ? ucap.p : nullptr;
+    a.bound_only = 0;
     const char* dbg = getenv("NNM_TC_DBG");
     a.dbg = dbg ? atoi(dbg) : 0;
     const int grid = (int)std::min<int64_t>(nfull, (int64_t)sms);
@@ -1879,6 +1895,16 @@ struct nnm_dataset {
       a.trace = trbuf.p;
     }
     CUDA_TRY(cudaEventRecord(ev0, st));
+    if (tc_cap_on && tc_bound_first) {
+      // bound pass over the same items: component caps from screened upper bounds
+      // (no exact work), then the exact pass below with every row threshold capped
+      TcArgs ab = a;
+      ab.bound_only = 1;
+      ab.trace = nullptr;
+      fill_u32(ucap.p, vn, 0x7f800000u);  // +inf
+      CUDA_TRY(launch_tc_scan(ab, grid, st));
+      note_launch();
+    }
     CUDA_TRY(launch_tc_scan(a, grid, st));
     note_launch();
     CUDA_TRY(cudaEventRecord(ev1, st));
@@ -2286,7 +2312,15 @@ struct nnm_dataset {
     fill_none(b1, vn);
     fill_none(b2, vn);
     const double pe0 = stats.pairs_evaluated;
+    // component caps (TC path): the phase-1 scan first runs a bound pass over its items,
+    // then both exact scans cap every row threshold by its component's upper bound, so
+    // only rows that can still hold their component's minimum edge take exact inserts
+    const char* cpe = getenv("NNM_TC_CAP");
+    tc_cap_on = tc_on && !(cpe && cpe[0] == '0');
+    if (tc_cap_on) ucap.ensure(vn);
+    tc_bound_first = tc_cap_on;
     if (n1 > 0) scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
+    tc_bound_first = false;
     if (rank != 0) stats.pairs_evaluated = pe0;  // replicated phase 1 counts once per job
     ucomp.ensure(vn);
     fill_none(ucomp.p, vn);
@@ -2298,6 +2332,7 @@ struct nnm_dataset {
     const int64_t lo2 = n2 * rank / world, hi2 = n2 * (rank + 1) / world;
     if (hi2 > lo2)
       scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, lo2, hi2, items2.p, false, tumax.p);
+    tc_cap_on = false;
     if (rank == 0) pairs_covered += (double)n * (double)(n - 1) / 2.0;
     const char* dbg_env = getenv("NNM_DEBUG");
     if (dbg_env && atoi(dbg_env) >= 2) {  // list statistics (expensive host copies)

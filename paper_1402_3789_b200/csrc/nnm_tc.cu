@@ -558,8 +558,18 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
     int prevI = -1;
     unsigned long long k1 = NONE_KEY, k2 = NONE_KEY;
     float gT = INFINITY, tup = INFINITY;  // tup: seeded upper bound of the second best
+    float capT = INFINITY;                // the component's cap (exact mode)
+    float rowU = INFINITY;                // best screened upper bound of the row (bound mode)
     int ci = -1;
     int64_t g = 0;
+    auto flush_row = [&]() {
+      if (ci < 0 || p.dump) return;
+      if (p.bound_only) {
+        if (p.ucap && rowU < INFINITY) atomicMin(p.ucap + ci, __float_as_uint(rowU));
+      } else {
+        insert_top2_g(p.B1 + g, p.B2 + g, k1, k2);
+      }
+    };
     for (int q = e; q < nq; q += TC_EPI_GROUPS) {
       const int s = q % TC_STAGES;
       if (tid == 0) trace(p, 6, q, 0);
@@ -568,14 +578,20 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
       const int2 it = S.ring[q % TC_RING];
       const int I = it.x, J = it.y;
       if (I != prevI) {
-        if (prevI >= 0 && ci >= 0 && !p.dump) insert_top2_g(p.B1 + g, p.B2 + g, k1, k2);
+        if (prevI >= 0) flush_row();
         prevI = I;
         g = (int64_t)I * TILE + i;
         ci = __ldg(p.comp + g);
-        const unsigned long long gb = *((volatile const unsigned long long*)(p.B2 + g));
-        gT = key_valid(gb) ? key_value(gb) : INFINITY;
+        if (p.bound_only) {
+          gT = INFINITY;
+        } else {
+          const unsigned long long gb = *((volatile const unsigned long long*)(p.B2 + g));
+          gT = key_valid(gb) ? key_value(gb) : INFINITY;
+        }
+        capT = (!p.bound_only && p.ucap && ci >= 0) ? __uint_as_float(p.ucap[ci]) : INFINITY;
         k1 = k2 = NONE_KEY;
         tup = INFINITY;
+        rowU = INFINITY;
       }
       const float r = S.rrow[s][i], Erow = S.erow[s][i], eta_row = S.etarow[s][i];
       // G' threshold equivalent to "L <= T may hold" (vthr: largest v with L <= T)
@@ -585,7 +601,8 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         const float vthr = (st * st + Erow) * 1.00001f;
         return (r - vthr) * 0.5f - (fabsf(r) + vthr) * 1e-6f - 1e-30f;
       };
-      float T = fminf(fminf(k2 == NONE_KEY ? INFINITY : key_value(k2), fminf(gT, tup)), p.thr_hi);
+      float T = fminf(fminf(k2 == NONE_KEY ? INFINITY : key_value(k2), fminf(gT, tup)),
+                      fminf(p.thr_hi, capT));
       float gam = gamma_of(T);
       const int a = q % TC_ACC;
       mbar_wait(&S.tfull[a], (q / TC_ACC) & 1);
@@ -596,6 +613,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         // levels of the reduction tree) -> bit mask of groups that may hold a candidate
         uint32_t gm = 0;
         float rmax = -INFINITY;  // largest G' of the row (tile-pair bound)
+        float gmax[16];          // 8-column group maxima (bound mode skips groups below b1)
 #pragma unroll 1
         for (int hb = 0; hb < 2; ++hb) {
           float v[64];
@@ -614,10 +632,38 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
                                      fmaxf(fmaxf(g8[4], g8[5]), fmaxf(g8[6], g8[7]))));
             uint32_t m = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) m |= (g8[k] >= gam) ? (1u << k) : 0u;
+            for (int k = 0; k < 8; ++k) {
+              m |= (g8[k] >= gam) ? (1u << k) : 0u;
+              gmax[8 * hb + k] = g8[k];
+            }
             gm |= (ci >= 0 ? m : 0u) << (8 * hb);
           }
         }
+        if (p.bound_only) {
+          // bound mode: the largest G' over the row's valid cross-component columns gives a
+          // real eligible-or-farther partner with S <= (sqrt(v + E) + eta)^2: the row's
+          // rigorous upper bound, min over the row tile's items, atomicMin into its
+          // component's cap at the end of the row tile (flush_row)
+          float b1 = -INFINITY;
+#pragma unroll 1
+          for (int gidx = 0; gidx < TILE / 8; ++gidx) {
+            if (!__any_sync(0xFFFFFFFFu, ci >= 0 && gmax[gidx] > b1)) continue;
+            float w[8];
+            tmem_ld8(lane_base + a * TILE + gidx * 8, w);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int cj = S.bcomp[s][gidx * 8 + u];
+              if (cj >= 0 && cj != ci) b1 = fmaxf(b1, w[u]);
+            }
+          }
+          if (ci >= 0 && b1 > -INFINITY) {
+            const double v1 = (double)__fmaf_rn(-2.f, b1, r);
+            const double e = (double)Erow * (1.0 + 1e-9) + 1.02 * 5.9604644775390625e-08 * fabs(v1);
+            const double up = sqrt(fmax(0.0, v1 + e)) * (1.0 + 1e-15) + (double)eta_row;
+            rowU = fminf(rowU, float_up(up * up * (1.0 + 1e-15)));
+          }
+          gm = 0;  // no exact work in bound mode
+        } else
         // threshold seed: a row with no finite threshold yet (first items of a row tile in
         // phase 1) would send every column to the FP64 path.  The two largest valid G' of the
         // item give two distinct eligible partners with S <= (sqrt(v + E) + eta)^2, so the
@@ -689,7 +735,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
               } else {
                 k2 = key;
               }
-              T = fminf(fminf(key_value(k2), fminf(gT, tup)), p.thr_hi);
+              T = fminf(fminf(key_value(k2), fminf(gT, tup)), fminf(p.thr_hi, capT));
               gam = gamma_of(T);
             }
           }
@@ -726,7 +772,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         mbar_arrive(&S.empty[s]);
       }
     }
-    if (prevI >= 0 && ci >= 0 && !p.dump) insert_top2_g(p.B1 + g, p.B2 + g, k1, k2);
+    if (prevI >= 0) flush_row();
   }
 
   tc_before();

@@ -33,6 +33,12 @@ struct TcArgs {
   unsigned* tpmin;        // [T(T+1)/2] per tile pair: fp32 bits of a lower bound of S over
                           // the pairs not masked same-component (atomicMax; nullptr: off)
   int dbg;                // timing experiments (NNM_TC_DBG): 1 = no epilogue work, 2 = no prep work
+  // component caps (DESIGN 3.1): [np] per component label, fp32 bits of a rigorous UPPER
+  // bound of the component's minimum cross edge.  bound_only: the scan writes them
+  // (atomicMin of each row's best screened upper bound; no exact work, no keys);
+  // otherwise every row threshold is capped by its component's value (nullptr: off)
+  unsigned* ucap;
+  int bound_only;
 };
 
 size_t tc_smem_bytes();
