@@ -1093,6 +1093,200 @@ __global__ void enum_write_kernel(const unsigned char* __restrict__ keep,
   }
 }
 
+// ---- per-dataset tile-pair tables (computed once per dataset and metric) -------------
+// Geometric lower bound of every tile pair (triangle index), fp32 rounded down: the
+// rounds' phase-2 enumeration then streams this table (and the tile-pair cache that
+// starts from it) instead of recomputing T(T+1)/2 centre distances every round.
+template <int M>
+__global__ void tile_glb_kernel(const float* __restrict__ c32, const float* __restrict__ cn,
+                                const float* __restrict__ r32, int T, int d,
+                                unsigned* __restrict__ glb) {
+  const int I0 = blockIdx.x * TR;
+  const int nr = min(TR, T - I0);
+  __shared__ __align__(16) float ci[TR][192];
+  for (int t = threadIdx.x; t < TR * d; t += blockDim.x) {
+    const int r = t / d, k = t % d;
+    ci[r][k] = r < nr ? c32[(int64_t)k * T + I0 + r] : 0.f;
+  }
+  __syncthreads();
+  for (int J = I0 + threadIdx.x; J < T; J += blockDim.x) {
+    float dc[TR];
+    cdist32_rows<M>(c32, T, ci, J, d, dc);
+    const float cnJ = cn[J], rJ = r32[J];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int I = I0 + r;
+      if (r >= nr || J < I) continue;
+      float lb = 0.f;
+      if (J != I) {
+        const double v = tile_lb32<M>(dc[r], cn[I], cnJ, r32[I], rJ, d);
+        lb = (v > 0.0) ? float_down(v) : 0.f;  // NaN -> 0 (keeps the pair)
+      }
+      glb[tri_index(T, I, J)] = __float_as_uint(lb);
+    }
+  }
+}
+
+// Phase-2 enumeration from the tile-pair bound table (one block per row tile I; columns
+// J >= I read contiguously): kept iff not a phase-1 item, not inside one component, and
+// the rigorous lower bound can reach either component bound (fail-safe on NaN).
+__global__ void enum_table_kernel(const unsigned* __restrict__ bnd, const int2* __restrict__ trange,
+                                  const double* __restrict__ umax, const unsigned* __restrict__ bits,
+                                  int T, unsigned char* __restrict__ keep, int* __restrict__ counts) {
+  const int I = blockIdx.x;
+  const int64_t w0 = tri_index(T, I, I);
+  const int2 tI = trange[I];
+  const double uI = umax[I];
+  int c = 0;
+  for (int J = I + threadIdx.x; J < T; J += blockDim.x) {
+    const int64_t w = w0 + (J - I);
+    const int2 tJ = trange[J];
+    bool k = !((bits[w >> 5] >> (w & 31)) & 1u) &&
+             !(tI.x == tI.y && tJ.x == tJ.y && tI.x == tJ.x);  // same_single(I, J)
+    if (k && J != I) k = !((double)__uint_as_float(bnd[w]) > fmax(uI, umax[J]));
+    keep[w] = k;
+    c += k;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  __shared__ int s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    counts[I] = t;
+  }
+}
+
+// Nearest tiles of every tile (phase-1 seed candidates), ranked as phase1_kernel does
+// (centre distance minus min(R_I, R_J), the tile itself first; ties: smaller J) but
+// without the per-round component filter: NBR_SLICE best per (tile, column slice), then
+// the NBR best per tile.  Each round then picks its seeds from this list.
+constexpr int NBR_SLICE = 16;
+constexpr int NBR = 32;
+
+template <int M, int D>
+__global__ void __launch_bounds__(P1_ROWS) tile_knn_kernel(const float* __restrict__ c32,
+                                                           const float* __restrict__ r32, int T,
+                                                           float* __restrict__ cand_l,
+                                                           int* __restrict__ cand_j) {
+  constexpr int d = D;
+  const int I = blockIdx.x * P1_ROWS + threadIdx.x;
+  const int chunk = blockIdx.y;
+  const int per = (T + P1_CHUNKS - 1) / P1_CHUNKS;
+  const int J0 = chunk * per, J1 = min(T, J0 + per);
+  __shared__ float sc[P1_JT][D + 1];
+  __shared__ float sr[P1_JT];
+  const bool live = I < T;
+  float ci[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) ci[k] = live ? __ldg(c32 + (int64_t)k * T + I) : 0.f;
+  const float rI = live ? r32[I] : 0.f;
+  float bl[NBR_SLICE];
+  int bj[NBR_SLICE];
+#pragma unroll
+  for (int k = 0; k < NBR_SLICE; ++k) {
+    bl[k] = INFINITY;
+    bj[k] = -1;
+  }
+  for (int Jb = J0; Jb < J1; Jb += P1_JT) {
+    const int nj = min(P1_JT, J1 - Jb);
+    __syncthreads();
+    for (int t = threadIdx.x; t < P1_JT * D; t += P1_ROWS) {
+      const int k = t / P1_JT, j = t % P1_JT;
+      sc[j][k] = j < nj ? __ldg(c32 + (int64_t)k * T + Jb + j) : 0.f;
+    }
+    if (threadIdx.x < P1_JT && threadIdx.x < nj) sr[threadIdx.x] = r32[Jb + threadIdx.x];
+    __syncthreads();
+    if (!live) continue;
+    for (int j = 0; j < nj; ++j) {
+      const int J = Jb + j;
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float t = fabsf(ci[k] - sc[j][k]);
+        if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc = fmaf(t, t, acc);
+        else if (M == MANHATTAN) acc += t;
+        else acc = fmaxf(acc, t);
+      }
+      const float dc = (M == EUCLIDEAN || M == SQEUCLIDEAN) ? sqrtf(acc) : acc;
+      float v = (J == I) ? -INFINITY : dc - fminf(sr[j], rI);
+      if (!(v < bl[NBR_SLICE - 1])) continue;
+      int jj = J;
+#pragma unroll
+      for (int k = 0; k < NBR_SLICE; ++k) {
+        if (v < bl[k]) {
+          const float tv = bl[k];
+          const int tj = bj[k];
+          bl[k] = v;
+          bj[k] = jj;
+          v = tv;
+          jj = tj;
+        }
+      }
+    }
+  }
+  if (!live) return;
+  const int64_t o = ((int64_t)I * P1_CHUNKS + chunk) * NBR_SLICE;
+#pragma unroll
+  for (int k = 0; k < NBR_SLICE; ++k) {
+    cand_l[o + k] = bl[k];
+    cand_j[o + k] = bj[k];
+  }
+}
+
+__global__ void tile_knn_merge_kernel(const float* __restrict__ cand_l, const int* __restrict__ cand_j,
+                                      int T, int* __restrict__ nbr) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= T) return;
+  const int64_t o = (int64_t)I * P1_CHUNKS * NBR_SLICE;
+  float bl[NBR];
+  int bj[NBR];
+#pragma unroll
+  for (int k = 0; k < NBR; ++k) {
+    bl[k] = INFINITY;
+    bj[k] = -1;
+  }
+  // chunks hold ascending J ranges: visiting them in order keeps ties on the smaller J
+  for (int c = 0; c < P1_CHUNKS * NBR_SLICE; ++c) {
+    int jj = cand_j[o + c];
+    if (jj < 0) continue;
+    float v = cand_l[o + c];
+    if (!(v < bl[NBR - 1])) continue;
+#pragma unroll
+    for (int k = 0; k < NBR; ++k) {
+      if (v < bl[k]) {
+        const float tv = bl[k];
+        const int tj = bj[k];
+        bl[k] = v;
+        bj[k] = jj;
+        v = tv;
+        jj = tj;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NBR; ++k) nbr[(int64_t)I * NBR + k] = bj[k];
+}
+
+// this round's seeds: the first pk tiles of I's list that can hold a cross-component pair
+// with I (fewer when the list runs out: the seed set is a heuristic, any choice is sound)
+__global__ void phase1_pick_kernel(const int* __restrict__ nbr, const int2* __restrict__ trange,
+                                   int T, int pk, int2* __restrict__ out) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= T) return;
+  const int2 tI = trange[I];
+  int c = 0;
+  for (int k = 0; k < NBR && c < pk; ++k) {
+    const int J = nbr[(int64_t)I * NBR + k];
+    if (J < 0) break;
+    const int2 tJ = trange[J];
+    if (tI.x == tI.y && tJ.x == tJ.y && tI.x == tJ.x) continue;  // same_single(I, J)
+    out[(int64_t)I * PK + c++] = make_int2(min(I, J), max(I, J));
+  }
+  for (; c < PK; ++c) out[(int64_t)I * PK + c] = make_int2(-1, -1);
+}
+
 __global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt,
                                   const int* __restrict__ tcount, unsigned long long* acc) {
   // real point pairs covered by a list of tile pairs (for the stats)
@@ -1624,6 +1818,11 @@ struct nnm_dataset {
   DevBuf<int2> items1, items2;
   DevBuf<float> p1_l;  // phase-1 per-slice candidates (phase1_reg_kernel)
   DevBuf<int> p1_j;
+  // per-dataset tile-pair tables (geom_metric): geometric lower bound per tile pair and
+  // the NBR nearest tiles of every tile (phase-1 seed candidates)
+  DevBuf<unsigned> glb;
+  DevBuf<int> nbr;
+  int glb_metric = -1, nbr_metric = -1;
   // per tile pair (triangle index): fp32 bits of a lower bound of S over its cross-component
   // pairs, written by the tensor-core scan, read by the phase-2 enumeration (0: unknown)
   DevBuf<unsigned> tpmin;
@@ -2075,7 +2274,12 @@ struct nnm_dataset {
     tpmin_on = tc_on && !(ce && ce[0] == '0') && tile_pairs() * 4 <= ((int64_t)4 << 30);
     if (tpmin_on) {
       tpmin.ensure(tile_pairs());
-      CUDA_TRY(cudaMemsetAsync(tpmin.p, 0, tile_pairs() * sizeof(unsigned), st));
+      // the cache starts from the geometric bounds (both are lower bounds of every pair)
+      if (glb_ready())
+        CUDA_TRY(cudaMemcpyAsync(tpmin.p, glb.p, tile_pairs() * sizeof(unsigned),
+                                 cudaMemcpyDeviceToDevice, st));
+      else
+        CUDA_TRY(cudaMemsetAsync(tpmin.p, 0, tile_pairs() * sizeof(unsigned), st));
     }
     bv_round = 0;
     bv_ncomp = n;
@@ -2216,6 +2420,56 @@ struct nnm_dataset {
       CUDA_TRY(cudaGetLastError());
     }
     geom_metric = kind;
+    build_tile_tables(kind);
+  }
+
+  bool glb_ready() const { return glb_metric >= 0 && glb_metric == geom_metric; }
+  bool nbr_ready() const { return nbr_metric >= 0 && nbr_metric == geom_metric; }
+
+  // per-dataset tile-pair tables (once per dataset and metric): the geometric lower bound
+  // of every tile pair (<= 2 GB) and the nearest-tile lists (d = 8 / 25)
+  void build_tile_tables(int kind) {
+    const int64_t W = (int64_t)Tp * (Tp + 1) / 2;
+    const char* te = getenv("NNM_TILE_TABLES");
+    const bool on = !(te && te[0] == '0');
+    glb_metric = nbr_metric = -1;
+    if (on && W * 4 <= ((int64_t)2 << 30)) {
+      glb.ensure(W);
+      const int g = (Tp + TR - 1) / TR;
+      switch (kind) {
+        case MANHATTAN: tile_glb_kernel<MANHATTAN><<<g, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, Tp, d, glb.p); break;
+        case CHEBYSHEV: tile_glb_kernel<CHEBYSHEV><<<g, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, Tp, d, glb.p); break;
+        default: tile_glb_kernel<EUCLIDEAN><<<g, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, Tp, d, glb.p);
+      }
+      note_launch();
+      CUDA_TRY(cudaGetLastError());
+      glb_metric = kind;
+    }
+    if (on && (d == 25 || d == 8)) {
+      p1_l.ensure((size_t)Tp * P1_CHUNKS * NBR_SLICE);
+      p1_j.ensure((size_t)Tp * P1_CHUNKS * NBR_SLICE);
+      nbr.ensure((size_t)Tp * NBR);
+      const dim3 g((Tp + P1_ROWS - 1) / P1_ROWS, P1_CHUNKS);
+#define NNM_KNN(MM, DD) tile_knn_kernel<MM, DD><<<g, P1_ROWS, 0, st>>>(tc32.p, tr32.p, Tp, p1_l.p, p1_j.p)
+      if (d == 25) {
+        switch (kind) {
+          case MANHATTAN: NNM_KNN(MANHATTAN, 25); break;
+          case CHEBYSHEV: NNM_KNN(CHEBYSHEV, 25); break;
+          default: NNM_KNN(EUCLIDEAN, 25);
+        }
+      } else {
+        switch (kind) {
+          case MANHATTAN: NNM_KNN(MANHATTAN, 8); break;
+          case CHEBYSHEV: NNM_KNN(CHEBYSHEV, 8); break;
+          default: NNM_KNN(EUCLIDEAN, 8);
+        }
+      }
+#undef NNM_KNN
+      note_launch();
+      tile_knn_merge_kernel<<<blocks_for(Tp), 256, 0, st>>>(p1_l.p, p1_j.p, Tp, nbr.p); note_launch();
+      CUDA_TRY(cudaGetLastError());
+      nbr_metric = kind;
+    }
   }
 
   template <int M>
@@ -2224,7 +2478,11 @@ struct nnm_dataset {
     // phase-1 seeds: PK nearest cross-capable tiles per tile
     items1.ensure((size_t)Tp * PK);
     const char* p1e = getenv("NNM_P1REG");
-    if ((d == 25 || d == 8) && !(p1e && p1e[0] == '0')) {
+    const char* pke0 = getenv("NNM_PK");
+    const int pk0 = pke0 ? std::max(1, std::min(PK, atoi(pke0))) : 4;
+    if (nbr_ready()) {
+      phase1_pick_kernel<<<blocks_for(Tp), 256, 0, st>>>(nbr.p, tile_range.p, Tp, pk0, items1.p); note_launch();
+    } else if ((d == 25 || d == 8) && !(p1e && p1e[0] == '0')) {
       p1_l.ensure((size_t)Tp * P1_CHUNKS * PK);
       p1_j.ensure((size_t)Tp * P1_CHUNKS * PK);
       const dim3 g((Tp + P1_ROWS - 1) / P1_ROWS, P1_CHUNKS);
@@ -2268,9 +2526,14 @@ struct nnm_dataset {
     pkeep.ensure(W);
     pcount.ensure(Tp);
     poffset.ensure(Tp + 1);
-    enum_count_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
-                                             Tp, d, tpmin_use ? tpmin.p : nullptr,
-                                             pkeep.p, pcount.p); note_launch();
+    if (glb_ready())
+      enum_table_kernel<<<Tp, 256, 0, st>>>(tpmin_use ? tpmin.p : glb.p, tile_range.p, tumax.p,
+                                            pbits.p, Tp, pkeep.p, pcount.p);
+    else
+      enum_count_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
+                                               Tp, d, tpmin_use ? tpmin.p : nullptr,
+                                               pkeep.p, pcount.p);
+    note_launch();
     CUDA_TRY(cudaGetLastError());
     thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), pcount.p, pcount.p + Tp, poffset.p, 0LL);
     long long last_off = read1(poffset.p + (Tp - 1));
