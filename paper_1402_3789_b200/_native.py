@@ -149,6 +149,21 @@ def check(rc: int) -> None:
     raise NativeError(rc, msg)
 
 
+_gpu_count = None
+
+
+def gpu_count() -> int:
+    """Number of usable sm_100 devices (0 when there is none; cached)."""
+    global _gpu_count
+    if _gpu_count is None:
+        c = ctypes.c_int32(0)
+        try:
+            _gpu_count = int(c.value) if load().nnm_device_count(ctypes.byref(c)) == NNM_OK else 0
+        except ImportError:
+            _gpu_count = 0
+    return _gpu_count
+
+
 def default_device() -> int:
     for var in ("NNM_DEVICE", "LOCAL_RANK"):
         v = os.environ.get(var)

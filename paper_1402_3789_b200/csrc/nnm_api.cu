@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
 #include <thrust/sort.h>
@@ -1369,10 +1370,12 @@ __global__ void kd_key_kernel(const double* __restrict__ X64, int64_t n, int d,
 constexpr int KD_SPLIT_THREADS = 256;
 __global__ void __launch_bounds__(KD_SPLIT_THREADS) kd_splitpos_kernel(const unsigned long long* __restrict__ keys,
                                    const int* __restrict__ sbeg, const int* __restrict__ ssz,
-                                   int nseg, int allow_off, int* __restrict__ ssplit) {
+                                   int nseg, int allow_off, int* __restrict__ ssplit,
+                                   int small_only) {
   const int sgm = blockIdx.x;
   if (sgm >= nseg) return;
   const int sz = ssz[sgm], b = sbeg[sgm];
+  if (small_only && sz > TILE) return;  // decided by kd_gap_split_kernel
   if (sz <= 1 || (sz <= TILE && !allow_off)) {
     if (threadIdx.x == 0) ssplit[sgm] = sz;
     return;
@@ -1447,6 +1450,77 @@ __global__ void __launch_bounds__(KD_SPLIT_THREADS) kd_splitpos_kernel(const uns
     else if (allow_off && ext > 0.f && bg2 >= 0.25f * ext) L = bp2;  // cut a separated piece off
     ssplit[sgm] = L;
   }
+}
+
+// Split search for the big top-level segments (few segments, millions of points): a
+// grid over the sorted positions computes every gap and reduces the two arg-max gaps
+// per segment (balanced range / anywhere; ties: smaller index) with packed 64-bit
+// atomicMax (gap bits << 32 | ~index), pre-reduced per block when the block lies inside
+// one segment; kd_gap_split_kernel then applies kd_splitpos_kernel's decision rule.
+__device__ __forceinline__ float kd_val(const unsigned long long* keys, int64_t p) {
+  uint32_t u = (uint32_t)(keys[p] & 0xFFFFFFFFull);
+  u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+  return __uint_as_float(u);
+}
+
+__global__ void kd_gap_kernel(const unsigned long long* __restrict__ keys, int64_t n,
+                              const int* __restrict__ segid, const int* __restrict__ sbeg,
+                              const int* __restrict__ ssz, unsigned long long* __restrict__ gbest) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long bal = 0, any = 0;
+  int sgm = -1;
+  if (p < n) {
+    sgm = segid[p];
+    const int b = sbeg[sgm], sz = ssz[sgm], i = (int)(p - b);
+    if (sz > TILE && i >= 1) {
+      const float g = kd_val(keys, p) - kd_val(keys, p - 1);
+      const unsigned long long pk = ((unsigned long long)__float_as_uint(fmaxf(g, 0.f)) << 32) |
+                                    (unsigned)(~(unsigned)i);
+      any = pk;
+      if (i >= sz / 4 && i <= sz - sz / 4) bal = pk;
+    }
+  }
+  const int s0 = __shfl_sync(0xFFFFFFFFu, sgm, 0);
+  const bool uniform = __all_sync(0xFFFFFFFFu, sgm == s0);
+  if (uniform) {  // warp inside one segment: reduce first
+    for (int o = 16; o > 0; o >>= 1) {
+      bal = max(bal, __shfl_xor_sync(0xFFFFFFFFu, bal, o));
+      any = max(any, __shfl_xor_sync(0xFFFFFFFFu, any, o));
+    }
+    if ((threadIdx.x & 31) == 0 && s0 >= 0) {
+      if (bal) atomicMax(gbest + 2 * s0, bal);
+      if (any) atomicMax(gbest + 2 * s0 + 1, any);
+    }
+  } else if (sgm >= 0) {
+    if (bal) atomicMax(gbest + 2 * sgm, bal);
+    if (any) atomicMax(gbest + 2 * sgm + 1, any);
+  }
+}
+
+__global__ void kd_gap_split_kernel(const unsigned long long* __restrict__ keys,
+                                    const int* __restrict__ sbeg, const int* __restrict__ ssz,
+                                    int nseg, int allow_off,
+                                    const unsigned long long* __restrict__ gbest,
+                                    int* __restrict__ ssplit) {
+  const int sgm = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sgm >= nseg) return;
+  const int sz = ssz[sgm], b = sbeg[sgm];
+  if (sz <= TILE) {  // small segments: kd_splitpos_kernel (never reached: routed there)
+    ssplit[sgm] = sz;
+    return;
+  }
+  const unsigned long long gb = gbest[2 * sgm], ga = gbest[2 * sgm + 1];
+  const float bg = gb ? __uint_as_float((unsigned)(gb >> 32)) : -1.f;
+  const int bp = gb ? (int)(~(unsigned)(gb & 0xFFFFFFFFull)) : sz / 2;
+  const float bg2 = ga ? __uint_as_float((unsigned)(ga >> 32)) : -1.f;
+  const int bp2 = ga ? (int)(~(unsigned)(ga & 0xFFFFFFFFull)) : sz / 2;
+  const float ext = kd_val(keys, b + sz - 1) - kd_val(keys, b);
+  int L = ((sz + TILE) / (2 * TILE)) * TILE;
+  if (L < TILE) L = TILE;
+  if (L > sz - 1) L = sz - 1;
+  if (ext > 0.f && bg >= 0.1f * ext) L = bp;
+  else if (allow_off && ext > 0.f && bg2 >= 0.25f * ext) L = bp2;  // cut a separated piece off
+  ssplit[sgm] = L;
 }
 
 __global__ void kd_children_kernel(int nseg, const int* __restrict__ ssz,
@@ -2319,8 +2393,9 @@ struct nnm_dataset {
       CUDA_TRY(cudaMemcpyAsync(segid.p, hseg.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
       sync();
     } else {
-      DevBuf<int> sdim, ssplit, nchild, cbase, nbeg, nsz;
-      DevBuf<unsigned long long> keys;
+      DevBuf<int> sdim, ssplit, nchild, cbase, nbeg, nsz, order2;
+      DevBuf<unsigned long long> keys, keys2, gbest;
+      DevBuf<char> kd_tmp;
       keys.ensure(n);
       for (int lv = 0; lv < 64; ++lv) {
         // separated pieces may be cut off anywhere (and leaves split at a clear gap) in the
@@ -2338,8 +2413,35 @@ struct nnm_dataset {
         cbase.ensure(nseg + 1);
         kd_dim_kernel<<<nseg, 32, 0, st>>>(X64.p, d, order.p, sbeg.p, ssz.p, nseg, allow_off, sdim.p); note_launch();
         kd_key_kernel<<<blocks_for(n), 256, 0, st>>>(X64.p, n, d, order.p, segid.p, sdim.p, keys.p); note_launch();
-        thrust::stable_sort_by_key(thrust::cuda::par(talloc).on(st), keys.p, keys.p + n, order.p);
-        kd_splitpos_kernel<<<nseg, KD_SPLIT_THREADS, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, allow_off, ssplit.p); note_launch();
+        // stable radix sort on (segment, coordinate): only the bits the segment ids use
+        {
+          int sbits = 0;
+          while (sbits < 31 && (1 << sbits) < nseg) ++sbits;
+          order2.ensure(n);
+          keys2.ensure(n);
+          size_t tb = 0;
+          cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys2.p, order.p, order2.p, (int)n, 0,
+                                          32 + sbits, st);
+          kd_tmp.ensure(tb);
+          CUDA_TRY(cub::DeviceRadixSort::SortPairs(kd_tmp.p, tb, keys.p, keys2.p, order.p, order2.p,
+                                                   (int)n, 0, 32 + sbits, st));
+          std::swap(keys.p, keys2.p);
+          std::swap(keys.n, keys2.n);
+          std::swap(order.p, order2.p);
+          std::swap(order.n, order2.n);
+        }
+        if (nseg < 2 * sms) {  // few big segments: the position-parallel split search
+          gbest.ensure(2 * nseg);
+          CUDA_TRY(cudaMemsetAsync(gbest.p, 0, 2 * nseg * sizeof(unsigned long long), st));
+          kd_gap_kernel<<<blocks_for(n), 256, 0, st>>>(keys.p, n, segid.p, sbeg.p, ssz.p, gbest.p); note_launch();
+          kd_gap_split_kernel<<<blocks_for(nseg), 256, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, allow_off,
+                                                                gbest.p, ssplit.p); note_launch();
+          // segments <= TILE in this level still take the leaf rule of kd_splitpos_kernel
+          kd_splitpos_kernel<<<nseg, KD_SPLIT_THREADS, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, allow_off,
+                                                                ssplit.p, 1); note_launch();
+        } else {
+          kd_splitpos_kernel<<<nseg, KD_SPLIT_THREADS, 0, st>>>(keys.p, sbeg.p, ssz.p, nseg, allow_off, ssplit.p, 0); note_launch();
+        }
         kd_children_kernel<<<blocks_for(nseg), 256, 0, st>>>(nseg, ssz.p, ssplit.p, nchild.p); note_launch();
         thrust::exclusive_scan(thrust::cuda::par(talloc).on(st), nchild.p, nchild.p + nseg, cbase.p, 0);
         int lastc = read1(nchild.p + (nseg - 1)), lastb = read1(cbase.p + (nseg - 1));
