@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define NNM_ABI_VERSION 2
+#define NNM_ABI_VERSION 3
 
 enum {
   NNM_OK = 0,
@@ -96,6 +96,15 @@ typedef struct {
   int64_t replay_gpu_merges; /* merges replayed on the GPU (nnm_replay.cu); the rest, if
                                 any, by the sequential host loop */
 } nnm_stats;
+
+typedef struct { /* per-round record of the last nnm_run on a dataset (SURVEY 5 observability) */
+  int64_t round;          /* 1-based: Boruvka round, or reference round on the round path */
+  double ms;              /* wall time of the round (host clock around synchronised work) */
+  double scan_ms;         /* CUDA-event time of the round's screening scans */
+  double pairs_evaluated; /* pairs the round's scans evaluated */
+  int64_t items;          /* tile pairs run through the tensor-core scan (0 on FP32 scans) */
+  int64_t merged;         /* MST edges added (Boruvka) / merges (round path) */
+} nnm_round_stat;
 
 int nnm_abi_version(void);
 const char *nnm_last_error(void);
@@ -168,6 +177,9 @@ int nnm_bv_finish_round(nnm_dataset *ds, const uint64_t *B1_dev, const uint64_t 
 /* sort + replay the accumulated edges into the merge log (kl1 truncation) */
 int nnm_bv_end(nnm_dataset *ds, int64_t kl1, nnm_merge *out_merges, int64_t *out_n_merges,
                int64_t *out_assign, int64_t *out_rounds, int32_t *out_stop, nnm_stats *stats);
+
+/* Per-round records of the last nnm_run on ds (*out_n = rounds recorded; at most cap copied). */
+int nnm_round_log(nnm_dataset *ds, nnm_round_stat *out, int64_t cap, int64_t *out_n);
 
 /* ---- CSV ingestion (dataio.py:49-116 load_dataset) ----
  * Parses a delimited text file with the reference's exact rules and messages:

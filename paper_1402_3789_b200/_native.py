@@ -26,7 +26,7 @@ NNM_E_UNSUPPORTED = -3
 NNM_E_NOMEM = -4
 NNM_E_CAPACITY = -5
 
-ABI_VERSION = 2  # include/nnm.h NNM_ABI_VERSION
+ABI_VERSION = 3  # include/nnm.h NNM_ABI_VERSION
 FLAG_ROUNDS = 1
 PATH_NAMES = {0: "none", 1: "boruvka", 2: "rounds"}
 STOP_NAMES = {1: "kl1-reached", 2: "no-eligible-pairs", 3: "single-cluster"}
@@ -37,7 +37,7 @@ EXPORTED = (
     "nnm_dataset_create_device", "nnm_dataset_destroy", "nnm_top_p", "nnm_run",
     "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_scan_pruned", "nnm_bv_second", "nnm_bv_finish_round",
     "nnm_bv_end", "nnm_measure_fp32_peak", "nnm_tc_probe", "nnm_csv_load", "nnm_csv_fetch",
-    "nnm_csv_free", "nnm_first_nonfinite", "nnm_bv_cache",
+    "nnm_csv_free", "nnm_first_nonfinite", "nnm_bv_cache", "nnm_round_log",
 )
 
 
@@ -60,6 +60,22 @@ class Stats(ctypes.Structure):
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["path"] = PATH_NAMES.get(self.path, str(self.path))
         return d
+
+
+class RoundStat(ctypes.Structure):
+    _fields_ = [("round", ctypes.c_int64), ("ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
+                ("pairs_evaluated", ctypes.c_double), ("items", ctypes.c_int64),
+                ("merged", ctypes.c_int64)]
+
+
+def round_log(handle) -> list:
+    """Per-round records of the last nnm_run on a dataset handle (nnm_round_log)."""
+    lib = load()
+    n = ctypes.c_int64()
+    check(lib.nnm_round_log(handle, None, 0, ctypes.byref(n)))
+    buf = (RoundStat * max(1, n.value))()
+    check(lib.nnm_round_log(handle, buf, n.value, ctypes.byref(n)))
+    return [{k: getattr(buf[i], k) for k, _ in RoundStat._fields_} for i in range(n.value)]
 
 
 MERGE_DTYPE = np.dtype([("round", np.int64), ("root_a", np.int64), ("root_b", np.int64),
@@ -123,6 +139,7 @@ def load():
         lib.nnm_bv_finish_round.argtypes = [vp, vp, vp, P(i64)]
         lib.nnm_bv_end.argtypes = [vp, i64, vp, P(i64), vp, P(i64), P(i32), P(Stats)]
         lib.nnm_measure_fp32_peak.argtypes = [i32, P(dbl)]
+        lib.nnm_round_log.argtypes = [vp, vp, i64, P(i64)]
         for name in EXPORTED:
             if name not in ("nnm_abi_version", "nnm_last_error"):
                 getattr(lib, name).restype = ctypes.c_int

@@ -32,6 +32,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/nnm.h"
 #include "nnm_common.cuh"
 #include "nnm_kernels.cuh"
@@ -171,6 +173,19 @@ struct PinnedBuf {  // grow-only page-locked host staging buffer (blocks from pi
     n = bytes / sizeof(T);
     return p;
   }
+};
+
+// NVTX ranges (header-only NVTX3: free unless a profiler attaches) per run / round / phase
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, long long v) {
+    char b[64];
+    snprintf(b, sizeof(b), fmt, v);
+    nvtxRangePushA(b);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 std::atomic<int64_t> g_launches{0};  // libnnm kernel launches (process-wide)
@@ -1921,7 +1936,26 @@ struct nnm_dataset {
   DevBuf<int> active, rmap, rsize;
   DevBuf<int2> kv;
   nnm_stats stats{};
+  std::vector<nnm_round_stat> round_log;  // per-round records of the last nnm_run
   CachedAlloc talloc;
+  // start / end of one round's record (stats deltas; the caller has synchronised)
+  nnm_round_stat rl_open(int64_t round) const {
+    nnm_round_stat r{};
+    r.round = round;
+    r.ms = -1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    r.scan_ms = -stats.scan_ms;
+    r.pairs_evaluated = -stats.pairs_evaluated;
+    r.items = -stats.tc_items;
+    return r;
+  }
+  void rl_close(nnm_round_stat r, int64_t merged) {
+    r.ms += 1e3 * std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    r.scan_ms += stats.scan_ms;
+    r.pairs_evaluated += stats.pairs_evaluated;
+    r.items += stats.tc_items;
+    r.merged = merged;
+    round_log.push_back(r);
+  }
 
   ~nnm_dataset() {
     // members (DevBuf) free asynchronously on st after this body; the stream is
@@ -2684,7 +2718,10 @@ struct nnm_dataset {
     tc_cap_on = tc_on && !(cpe && cpe[0] == '0');
     if (tc_cap_on) ucap.ensure(vn);
     tc_bound_first = tc_cap_on;
-    if (n1 > 0) scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
+    {
+      NvtxRange r1("nnm phase-1 scan (bound + exact)");
+      if (n1 > 0) scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
+    }
     tc_bound_first = false;
     if (rank != 0) stats.pairs_evaluated = pe0;  // replicated phase 1 counts once per job
     ucomp.ensure(vn);
@@ -2695,6 +2732,7 @@ struct nnm_dataset {
       default: ucomp_t<EUCLIDEAN>(b1); pruned_phase2<EUCLIDEAN>(n2);
     }
     const int64_t lo2 = n2 * rank / world, hi2 = n2 * (rank + 1) / world;
+    NvtxRange r2("nnm phase-2 scan");
     if (hi2 > lo2)
       scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, lo2, hi2, items2.p, false, tumax.p);
     tc_cap_on = false;
@@ -2750,6 +2788,7 @@ struct nnm_dataset {
   }
 
   int64_t bv_finish_round(const unsigned long long* b1, const unsigned long long* b2) {
+    NvtxRange nv("nnm finish round (refine, component minima, hook, jump)");
     const int N = (int)vn;  // positions of the Boruvka view (pads carry comp -1)
     ++bv_round;
     // counters[0]: edges (cumulative), [1]: ambiguous, [2]: rescan rows
@@ -2816,6 +2855,7 @@ struct nnm_dataset {
   // exceeds lmax -- and everything after it -- is finished by the sequential host loop.
   void bv_end(int64_t kl1, nnm_merge* out, int64_t* n_merges, int64_t* assign, int64_t* rounds,
               int32_t* stop) {
+    NvtxRange nv("nnm merge replay");
     const unsigned long long ne = read1(counters.p);
     auto stop_of = [&](int64_t c) -> int {
       if (c == 1) return NNM_STOP_SINGLE_CLUSTER;
@@ -3342,6 +3382,17 @@ int nnm_first_nonfinite(const double* X, int64_t count, int32_t threads, int64_t
   });
 }
 
+int nnm_round_log(nnm_dataset* ds, nnm_round_stat* out, int64_t cap, int64_t* out_n) {
+  return guarded([&] {
+    if (!ds || !out_n) invalid("null argument");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    const int64_t k = (int64_t)ds->round_log.size();
+    *out_n = k;
+    if (out)
+      for (int64_t i = 0; i < std::min(k, cap); ++i) out[i] = ds->round_log[i];
+  });
+}
+
 int nnm_dataset_destroy(nnm_dataset* ds) {
   return guarded([&] {
     if (!ds) return;
@@ -3422,6 +3473,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
     auto t0 = std::chrono::steady_clock::now();
     const int64_t launches0 = g_launches.load();
     ds->stats = nnm_stats{};
+    ds->round_log.clear();
     ds->pairs_covered = 0.0;
     ds->stats.device = ds->device;
     const int64_t n = ds->n;
@@ -3449,14 +3501,19 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
             if (th.joinable()) th.join();
         }
       } joiner{prefault};
-      ds->bv_begin(metric, cons->dmax);
-      ds->sync();
+      {
+        NvtxRange nv("nnm prep (view, geometry, tables)");
+        ds->bv_begin(metric, cons->dmax);
+        ds->sync();
+      }
       ds->stats.prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count();
       bool need = n > 1 && !(cons->kl1 > 0 && n <= cons->kl1);
       const char* pe = getenv("NNM_PRUNE");
       const bool prune = !(pe && pe[0] == '0');
       const bool dbg_t = getenv("NNM_DEBUG") != nullptr;
       while (need && ds->bv_ncomp > 1) {
+        NvtxRange nv("nnm boruvka round %lld", (long long)ds->bv_round + 1);
+        const nnm_round_stat rl = ds->rl_open(ds->bv_round + 1);
         auto th0 = std::chrono::steady_clock::now();
         if (prune) {
           ds->pruned_scan(metric);
@@ -3472,6 +3529,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
         }
         auto th1 = std::chrono::steady_clock::now();
         int64_t added = ds->bv_finish_round(ds->B1.p, ds->B2.p);
+        ds->rl_close(rl, added);
         if (dbg_t)
           fprintf(stderr, "[nnm] host: round finish %.2f ms\n",
                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th1).count());
@@ -3517,6 +3575,8 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       for (;;) {
         if (count == 1) { reason = NNM_STOP_SINGLE_CLUSTER; break; }
         if (kl1 > 0 && count <= kl1) { reason = NNM_STOP_KL1; break; }
+        NvtxRange nv("nnm round %lld", (long long)rounds + 1);
+        const nnm_round_stat rl = ds->rl_open(rounds + 1);
         ds->top_p(metric, thr, clamp_int(kl2, ds->n), clamp_int(kl3, ds->n), P, buf, rounds > 0);
         if (buf.empty()) { reason = NNM_STOP_NO_ELIGIBLE; break; }
         ++rounds;
@@ -3565,6 +3625,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
             break;
           }
         }
+        ds->rl_close(rl, merged);
         if (out_counters && n_counters < counters_cap) {
           nnm_round_counters& rc = out_counters[n_counters];
           rc.round = rounds;

@@ -172,8 +172,10 @@ def run_arrays(ddata, constraints: ConstraintSet, P: int, metric: MetricKind,
                               merges.ctypes.data, ctypes.byref(nm), assign.ctypes.data,
                               ctypes.byref(rounds), ctypes.byref(stop), counters.ctypes.data, ccap,
                               ctypes.byref(nc), ctypes.byref(st)))
+    stats = st.as_dict()
+    stats["round_log"] = _native.round_log(ddata.handle)
     return (merges[: nm.value], assign, rounds.value, _native.STOP_NAMES[stop.value],
-            counters[: min(nc.value, ccap)], st.as_dict())
+            counters[: min(nc.value, ccap)], stats)
 
 
 def run(dataset: Dataset, config: RunConfig) -> RunResult:
