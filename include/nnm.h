@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define NNM_ABI_VERSION 3
+#define NNM_ABI_VERSION 4
 
 enum {
   NNM_OK = 0,
@@ -155,19 +155,31 @@ int nnm_bv_begin(nnm_dataset *ds, int32_t metric, double dmax, int64_t *out_tile
                  int64_t *out_rows);
 int nnm_bv_scan(nnm_dataset *ds, int64_t w_begin, int64_t w_end, uint64_t *B1_dev,
                 uint64_t *B2_dev);
-/* Pruned round scan: every rank evaluates the small phase-1 item
- * list in full (so all ranks derive identical component bounds with no exchange)
- * and its contiguous 1/world share of the phase-2 items; keys land in (B1, B2).
- * world == 1 is the whole single-GPU pruned scan. */
-/* Tile-pair bound cache of the staged Boruvka run (valid after nnm_bv_begin): device
- * pointer and count of the per-tile-pair uint32 lower bounds (fp32 bits, 0 = unknown;
- * NULL / 0 when off: non-TC metric, or NNM_TPCACHE=0).  synced = 1 declares that the
- * caller all-reduces the array with MAX (as int32 or uint32: the bits of non-negative
- * floats) across ranks after every nnm_bv_scan_pruned; only then do multi-rank pruned
- * scans use it (every rank must derive the same phase-2 list). */
-int nnm_bv_cache(nnm_dataset *ds, int32_t synced, void **out_ptr, int64_t *out_count);
-int nnm_bv_scan_pruned(nnm_dataset *ds, int32_t rank, int32_t world, uint64_t *B1_dev,
-                       uint64_t *B2_dev);
+/* Staged pruned round (replaces scheduler.run_round's single manager pass
+ * for one Boruvka round, scheduler.py:268-335).  Rank r of `world` scans a contiguous
+ * 1/world share of each phase's tile-pair items; the caller combines between steps:
+ *   1. nnm_bv_round_bound: phase-1 item list (identical on every rank) and the bound pass
+ *      over this rank's share -> *out_caps (device, *out_count uint32 = fp32 bits of each
+ *      component's upper bound; NULL / 0 off the tensor-core path).  Caller: all-reduce
+ *      MIN (as int32: non-negative float bits order as integers).
+ *   2. nnm_bv_round_phase1(caps = the combined array, NULL: this rank's own): exact
+ *      phase-1 scan of the share -> (B1, B2).  Caller: G1 = min_r B1_r, G2 = min_r
+ *      nnm_bv_second(...) (two all-reduce MIN).
+ *   3. nnm_bv_round_phase2(G1, G2): component bounds from the combined keys, phase-2 list
+ *      (identical on every rank), (B1, B2) = (G1, G2) plus this rank's phase-2 share;
+ *      *out_cache / *out_count: this round's tile-pair cache entries (uint32, NULL / 0
+ *      when world == 1 or the cache is off).  Caller: all-reduce MAX of the cache buffer,
+ *      then nnm_bv_cache_scatter (required before the next round's step 1), and the key
+ *      combine again -> nnm_bv_finish_round(G1, G2).
+ * Steps out of order raise NNM_E_INVALID. */
+int nnm_bv_round_bound(nnm_dataset *ds, int32_t rank, int32_t world, uint32_t **out_caps,
+                       int64_t *out_count);
+int nnm_bv_round_phase1(nnm_dataset *ds, int32_t rank, int32_t world, const uint32_t *caps_dev,
+                        uint64_t *B1_dev, uint64_t *B2_dev);
+int nnm_bv_round_phase2(nnm_dataset *ds, int32_t rank, int32_t world, const uint64_t *G1_dev,
+                        const uint64_t *G2_dev, uint64_t *B1_dev, uint64_t *B2_dev,
+                        uint32_t **out_cache, int64_t *out_count);
+int nnm_bv_cache_scatter(nnm_dataset *ds);
 /* B2 contribution for the global second-best: B2c[i] = (B1loc[i] == B1glob[i]) ? B2loc[i] : B1loc[i] */
 int nnm_bv_second(nnm_dataset *ds, const uint64_t *B1loc_dev, const uint64_t *B2loc_dev,
                   const uint64_t *B1glob_dev, uint64_t *B2c_dev);
@@ -177,6 +189,18 @@ int nnm_bv_finish_round(nnm_dataset *ds, const uint64_t *B1_dev, const uint64_t 
 /* sort + replay the accumulated edges into the merge log (kl1 truncation) */
 int nnm_bv_end(nnm_dataset *ds, int64_t kl1, nnm_merge *out_merges, int64_t *out_n_merges,
                int64_t *out_assign, int64_t *out_rounds, int32_t *out_stop, nnm_stats *stats);
+
+/* Single-process multi-GPU run (engine.run with RunConfig.n_gpus > 1): one dataset
+ * replica per device (several replicas may share a device), the staged pruned round over
+ * 1/n_rep shares with the exchanges done by kernels reading the other replicas' buffers
+ * through peer memory (NVLink / NVSwitch).  Outputs and errors as nnm_run; the round
+ * path (kl2 / kl3 / kl4) runs on replicas[0] alone.  Results are byte-identical to
+ * nnm_run on one replica. */
+int nnm_run_multi(nnm_dataset **replicas, int32_t n_replicas, int32_t metric,
+                  const nnm_constraints *constraints, int64_t pairs_per_batch, int32_t flags,
+                  nnm_merge *out_merges, int64_t *out_n_merges, int64_t *out_assign,
+                  int64_t *out_rounds, int32_t *out_stop, nnm_round_counters *out_counters,
+                  int64_t counters_cap, int64_t *out_n_counters, nnm_stats *stats);
 
 /* Per-round records of the last nnm_run on ds (*out_n = rounds recorded; at most cap copied). */
 int nnm_round_log(nnm_dataset *ds, nnm_round_stat *out, int64_t cap, int64_t *out_n);

@@ -26,7 +26,7 @@ NNM_E_UNSUPPORTED = -3
 NNM_E_NOMEM = -4
 NNM_E_CAPACITY = -5
 
-ABI_VERSION = 3  # include/nnm.h NNM_ABI_VERSION
+ABI_VERSION = 4  # include/nnm.h NNM_ABI_VERSION
 FLAG_ROUNDS = 1
 PATH_NAMES = {0: "none", 1: "boruvka", 2: "rounds"}
 STOP_NAMES = {1: "kl1-reached", 2: "no-eligible-pairs", 3: "single-cluster"}
@@ -35,9 +35,10 @@ STOP_NAMES = {1: "kl1-reached", 2: "no-eligible-pairs", 3: "single-cluster"}
 EXPORTED = (
     "nnm_abi_version", "nnm_last_error", "nnm_device_count", "nnm_dataset_create",
     "nnm_dataset_create_device", "nnm_dataset_destroy", "nnm_top_p", "nnm_run",
-    "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_scan_pruned", "nnm_bv_second", "nnm_bv_finish_round",
+    "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_round_bound", "nnm_bv_round_phase1",
+    "nnm_bv_round_phase2", "nnm_bv_cache_scatter", "nnm_bv_second", "nnm_bv_finish_round",
     "nnm_bv_end", "nnm_measure_fp32_peak", "nnm_tc_probe", "nnm_csv_load", "nnm_csv_fetch",
-    "nnm_csv_free", "nnm_first_nonfinite", "nnm_bv_cache", "nnm_round_log",
+    "nnm_csv_free", "nnm_first_nonfinite", "nnm_round_log", "nnm_run_multi",
 )
 
 
@@ -127,14 +128,18 @@ def load():
         lib.nnm_pairwise.argtypes = [i32, vp, i64, vp, i64, i32, i32, vp]
         lib.nnm_bv_begin.argtypes = [vp, i32, dbl, P(i64), P(i64)]
         lib.nnm_bv_scan.argtypes = [vp, i64, i64, vp, vp]
-        lib.nnm_bv_scan_pruned.argtypes = [vp, i32, i32, vp, vp]
+        lib.nnm_bv_round_bound.argtypes = [vp, i32, i32, vp, P(i64)]
+        lib.nnm_bv_round_phase1.argtypes = [vp, i32, i32, vp, vp, vp]
+        lib.nnm_bv_round_phase2.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, P(i64)]
+        lib.nnm_bv_cache_scatter.argtypes = [vp]
+        lib.nnm_run_multi.argtypes = [vp, i32, i32, P(Constraints), i64, i32, vp, P(i64), vp,
+                                      P(i64), P(i32), vp, i64, P(i64), P(Stats)]
         lib.nnm_tc_probe.argtypes = [vp, vp, i64, P(dbl)]
         lib.nnm_csv_load.argtypes = [ctypes.c_char_p, ctypes.c_char, ctypes.c_char_p, i32, P(vp),
                                      P(i64), P(i64), P(i32), P(i64)]
         lib.nnm_csv_fetch.argtypes = [vp, vp, vp, vp]
         lib.nnm_csv_free.argtypes = [vp]
         lib.nnm_first_nonfinite.argtypes = [vp, i64, i32, P(i64)]
-        lib.nnm_bv_cache.argtypes = [vp, i32, P(vp), P(i64)]
         lib.nnm_bv_second.argtypes = [vp, vp, vp, vp, vp]
         lib.nnm_bv_finish_round.argtypes = [vp, vp, vp, P(i64)]
         lib.nnm_bv_end.argtypes = [vp, i64, vp, P(i64), vp, P(i64), P(i32), P(Stats)]

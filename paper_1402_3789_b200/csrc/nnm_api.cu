@@ -1303,6 +1303,23 @@ __global__ void phase1_pick_kernel(const int* __restrict__ nbr, const int2* __re
   for (; c < PK; ++c) out[(int64_t)I * PK + c] = make_int2(-1, -1);
 }
 
+// tile-pair cache entries of an item list <-> a compact buffer (multi-rank exchange)
+__global__ void cache_gather_kernel(const int2* __restrict__ items, int64_t cnt, int T,
+                                    const unsigned* __restrict__ tpmin, unsigned* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int2 it = items[t];
+  out[t] = tpmin[tri_index(T, min(it.x, it.y), max(it.x, it.y))];
+}
+
+__global__ void cache_scatter_kernel(const int2* __restrict__ items, int64_t cnt, int T,
+                                     const unsigned* __restrict__ in, unsigned* __restrict__ tpmin) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int2 it = items[t];
+  tpmin[tri_index(T, min(it.x, it.y), max(it.x, it.y))] = in[t];
+}
+
 __global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt,
                                   const int* __restrict__ tcount, unsigned long long* acc) {
   // real point pairs covered by a list of tile pairs (for the stats)
@@ -1916,12 +1933,11 @@ struct nnm_dataset {
   // pairs, written by the tensor-core scan, read by the phase-2 enumeration (0: unknown)
   DevBuf<unsigned> tpmin;
   // component caps (TC scan): bound pass over the phase-1 items, then capped exact scans
-  DevBuf<unsigned> ucap;
-  bool tc_cap_on = false;      // caps in use for this round's scans
-  bool tc_bound_first = false; // the next tc_scan runs the bound pass first (phase 1)
+  DevBuf<unsigned> ucap;        // this rank's caps from its bound-pass share (u32 fp32 bits)
+  bool tc_cap_on = false;       // caps in use for this round's scans
+  bool tc_bound_only = false;   // the next tc_scan is the bound pass (writes ucap, no keys)
   bool tpmin_on = false;   // allocated and reset for this run
   bool tpmin_use = false;  // this scan may read / write it
-  bool tpmin_sync = false; // multi-rank caller all-reduces (MAX) the cache after every scan
   DevBuf<unsigned> pbits;
   DevBuf<unsigned char> pkeep;
   DevBuf<int> pcount;
@@ -2188,8 +2204,8 @@ struct nnm_dataset {
     a.B2 = b2;
     a.dump = nullptr;
     a.tpmin = tpmin_use ? tpmin.p : nullptr;
-    a.ucap = tc_cap_on ? ucap.p : nullptr;
-    a.bound_only = 0;
+    a.ucap = tc_bound_only ? ucap.p : (tc_cap_on ? const_cast<unsigned*>(caps_read) : nullptr);
+    a.bound_only = tc_bound_only ? 1 : 0;
     const char* dbg = getenv("NNM_TC_DBG");
     a.dbg = dbg ? atoi(dbg) : 0;
     const int grid = (int)std::min<int64_t>(nfull, (int64_t)sms);
@@ -2202,16 +2218,6 @@ struct nnm_dataset {
       a.trace = trbuf.p;
     }
     CUDA_TRY(cudaEventRecord(ev0, st));
-    if (tc_cap_on && tc_bound_first) {
-      // bound pass over the same items: component caps from screened upper bounds
-      // (no exact work), then the exact pass below with every row threshold capped
-      TcArgs ab = a;
-      ab.bound_only = 1;
-      ab.trace = nullptr;
-      fill_u32(ucap.p, vn, 0x7f800000u);  // +inf
-      CUDA_TRY(launch_tc_scan(ab, grid, st));
-      note_launch();
-    }
     CUDA_TRY(launch_tc_scan(a, grid, st));
     note_launch();
     CUDA_TRY(cudaEventRecord(ev1, st));
@@ -2242,6 +2248,7 @@ struct nnm_dataset {
         fclose(f);
       }
     }
+    if (tc_bound_only) return;  // the exact pass over the same items counts the pairs
     counters.ensure(8);
     CUDA_TRY(cudaMemsetAsync(counters.p + 7, 0, sizeof(unsigned long long), st));
     item_pairs_kernel<<<blocks_for(n_up), 256, 0, st>>>(items + w_begin, n_up, cur_tcount, counters.p + 7); note_launch();
@@ -2378,7 +2385,6 @@ struct nnm_dataset {
     // tile-pair bound cache (TC scan only; 4 B per tile pair: 0.58 GB at 2M points)
     const char* ce = getenv("NNM_TPCACHE");
     tpmin_use = false;
-    tpmin_sync = false;
     tpmin_on = tc_on && !(ce && ce[0] == '0') && tile_pairs() * 4 <= ((int64_t)4 << 30);
     if (tpmin_on) {
       tpmin.ensure(tile_pairs());
@@ -2686,57 +2692,128 @@ struct nnm_dataset {
   }
 
   // One pruned Boruvka scan: exact per-row keys for every row that can hold its
-  // component's minimum edge.
-  void pruned_scan(int metric) { pruned_scan_shard(metric, B1.p, B2.p, 0, 1); }
+  // component's minimum edge; the single-rank sequence of the
+  // staged round steps below (no exchanges).
+  void pruned_scan(int metric) {
+    round_bound(metric, 0, 1);
+    round_phase1(B1.p, B2.p, 0, 1);
+    round_phase2(B1.p, B2.p, B1.p, B2.p, 0, 1);
+  }
 
-  // Pruned scan into (b1, b2) where this rank evaluates the phase-1 items in full
-  // (small, replicated so every rank derives the same component bounds without an
-  // exchange) and its contiguous share [lo, hi) of the phase-2 items.  With world
-  // == 1 this is the whole pruned scan.  Phase-1 pairs are counted on rank 0 only.
-  void pruned_scan_shard(int metric, unsigned long long* b1, unsigned long long* b2, int rank,
-                         int world) {
+  // ---- staged pruned round (DESIGN 6): every step is rank-local; between steps the
+  // caller combines across ranks (torch.distributed / NCCL, or nnm_run_multi's peer
+  // kernels).  Items of both phases are split into contiguous 1/world shares.
+  //   round_bound   phase-1 list (identical on every rank), bound pass over the share
+  //                 -> ucap (caller: all-reduce MIN -> caps)            [TC path only]
+  //   round_phase1  exact phase-1 scan of the share under the caps -> (b1, b2)
+  //                 (caller: min-combine of the keys -> (g1, g2))
+  //   round_phase2  component bounds from (g1, g2), phase-2 list (identical on every
+  //                 rank), (g1, g2) -> (b1, b2), exact scan of the share on top; the
+  //                 tile-pair cache entries of this round's items gathered into a compact
+  //                 buffer (caller: all-reduce MAX, then cache_scatter; min-combine of the
+  //                 keys) -> finish_round
+  int64_t rd_n1 = 0, rd_n2 = 0;
+  int rd_stage = 0;  // 0 idle, 1 bound done, 2 phase 1 done, 3 phase 2 done (cache pending)
+  const unsigned* caps_read = nullptr;  // caps the exact passes read (nullptr: none)
+  DevBuf<unsigned> cachebuf;            // compact tile-pair cache entries of this round
+  DevBuf<unsigned long long> G1, G2;    // combined keys (nnm_run_multi)
+  DevBuf<unsigned> ucapg, cacheg;       // combined caps / cache entries (nnm_run_multi)
+
+  static std::pair<int64_t, int64_t> share(int64_t total, int rank, int world) {
+    return {total * rank / world, total * (rank + 1) / world};
+  }
+
+  void round_bound(int metric, int rank, int world) {
+    if (world > 1 && rd_stage == 3)
+      throw NnmError{NNM_E_INVALID, "staged round: the tile-pair cache of the previous round was "
+                                    "not exchanged (nnm_bv_cache_scatter)"};
     ensure_geometry(metric);
-    // every rank must derive the same phase-2 list: the cache holds rank-local bounds of
-    // the phase-2 items, so a multi-rank scan uses it only when the caller all-reduces it
-    // (MAX) after every scan (nnm_bv_cache); the phase-1 writes are identical on all ranks
-    tpmin_use = tpmin_on && (world == 1 || tpmin_sync);
+    tpmin_use = tpmin_on;  // exchanged every round (compact MAX), so consistent on all ranks
     tile_range.ensure(Tp);
     tile_range_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, Tp, tile_range.p); note_launch();
-    int64_t n1 = 0, n2 = 0;
+    int64_t n2 = 0;
     switch (metric) {
-      case MANHATTAN: pruned_lists<MANHATTAN>(n1, n2); break;
-      case CHEBYSHEV: pruned_lists<CHEBYSHEV>(n1, n2); break;
-      default: pruned_lists<EUCLIDEAN>(n1, n2);
+      case MANHATTAN: pruned_lists<MANHATTAN>(rd_n1, n2); break;
+      case CHEBYSHEV: pruned_lists<CHEBYSHEV>(rd_n1, n2); break;
+      default: pruned_lists<EUCLIDEAN>(rd_n1, n2);
     }
-    fill_none(b1, vn);
-    fill_none(b2, vn);
-    const double pe0 = stats.pairs_evaluated;
-    // component caps (TC path): the phase-1 scan first runs a bound pass over its items,
-    // then both exact scans cap every row threshold by its component's upper bound, so
+    // component caps (TC path): the bound pass over this rank's phase-1 share; both exact
+    // scans then cap every row threshold by its component's (combined) upper bound, so
     // only rows that can still hold their component's minimum edge take exact inserts
     const char* cpe = getenv("NNM_TC_CAP");
     tc_cap_on = tc_on && !(cpe && cpe[0] == '0');
-    if (tc_cap_on) ucap.ensure(vn);
-    tc_bound_first = tc_cap_on;
-    {
-      NvtxRange r1("nnm phase-1 scan (bound + exact)");
-      if (n1 > 0) scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, 0, n1, p1_list, false);
+    caps_read = nullptr;
+    if (tc_cap_on) {
+      ucap.ensure(vn);
+      fill_u32(ucap.p, vn, 0x7f800000u);  // +inf
+      const auto sh = share(rd_n1, rank, world);
+      NvtxRange r0("nnm phase-1 bound pass");
+      tc_bound_only = true;
+      if (sh.second > sh.first)
+        scan(metric, B1.p, B2.p, true, INT_UNSET, INT_UNSET, bv_thr_hi, sh.first, sh.second, p1_list,
+             false);
+      tc_bound_only = false;
+      caps_read = ucap.p;  // single rank: the local caps are the global ones
     }
-    tc_bound_first = false;
-    if (rank != 0) stats.pairs_evaluated = pe0;  // replicated phase 1 counts once per job
+    rd_stage = 1;
+  }
+
+  void round_phase1(unsigned long long* b1, unsigned long long* b2, int rank, int world) {
+    if (rd_stage != 1) throw NnmError{NNM_E_INVALID, "staged round: phase 1 before the bound step"};
+    fill_none(b1, vn);
+    fill_none(b2, vn);
+    const auto sh = share(rd_n1, rank, world);
+    NvtxRange r1("nnm phase-1 scan");
+    if (sh.second > sh.first)
+      scan(bv_metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, sh.first, sh.second, p1_list,
+           false);
+    rd_stage = 2;
+  }
+
+  void round_phase2(const unsigned long long* g1, const unsigned long long* g2,
+                    unsigned long long* b1, unsigned long long* b2, int rank, int world) {
+    if (rd_stage != 2) throw NnmError{NNM_E_INVALID, "staged round: phase 2 before phase 1"};
+    if (b1 != g1) CUDA_TRY(cudaMemcpyAsync(b1, g1, vn * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+    if (b2 != g2) CUDA_TRY(cudaMemcpyAsync(b2, g2, vn * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
     ucomp.ensure(vn);
     fill_none(ucomp.p, vn);
-    switch (metric) {
-      case MANHATTAN: ucomp_t<MANHATTAN>(b1); pruned_phase2<MANHATTAN>(n2); break;
-      case CHEBYSHEV: ucomp_t<CHEBYSHEV>(b1); pruned_phase2<CHEBYSHEV>(n2); break;
-      default: ucomp_t<EUCLIDEAN>(b1); pruned_phase2<EUCLIDEAN>(n2);
+    switch (bv_metric) {
+      case MANHATTAN: ucomp_t<MANHATTAN>(b1); pruned_phase2<MANHATTAN>(rd_n2); break;
+      case CHEBYSHEV: ucomp_t<CHEBYSHEV>(b1); pruned_phase2<CHEBYSHEV>(rd_n2); break;
+      default: ucomp_t<EUCLIDEAN>(b1); pruned_phase2<EUCLIDEAN>(rd_n2);
     }
-    const int64_t lo2 = n2 * rank / world, hi2 = n2 * (rank + 1) / world;
-    NvtxRange r2("nnm phase-2 scan");
-    if (hi2 > lo2)
-      scan(metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, lo2, hi2, items2.p, false, tumax.p);
+    const auto sh = share(rd_n2, rank, world);
+    {
+      NvtxRange r2("nnm phase-2 scan");
+      if (sh.second > sh.first)
+        scan(bv_metric, b1, b2, true, INT_UNSET, INT_UNSET, bv_thr_hi, sh.first, sh.second, items2.p,
+             false, tumax.p);
+    }
     tc_cap_on = false;
     if (rank == 0) pairs_covered += (double)n * (double)(n - 1) / 2.0;
+    rd_stage = 0;
+    if (world > 1 && tpmin_use && rd_n1 + rd_n2 > 0) {
+      // this round's scanned items (identical lists on every rank) -> compact cache buffer
+      cachebuf.ensure(rd_n1 + rd_n2);
+      cache_gather_kernel<<<blocks_for(rd_n1), 256, 0, st>>>(p1_list, rd_n1, Tp, tpmin.p, cachebuf.p); note_launch();
+      if (rd_n2 > 0) { cache_gather_kernel<<<blocks_for(rd_n2), 256, 0, st>>>(items2.p, rd_n2, Tp, tpmin.p, cachebuf.p + rd_n1); note_launch(); }
+      CUDA_TRY(cudaGetLastError());
+      rd_stage = 3;
+    }
+    debug_lists(rd_n1, rd_n2);
+  }
+
+  // after the caller's all-reduce(MAX) of cachebuf: every rank holds the same cache
+  void cache_scatter(const unsigned* src = nullptr) {
+    if (rd_stage != 3) return;
+    if (!src) src = cachebuf.p;
+    cache_scatter_kernel<<<blocks_for(rd_n1), 256, 0, st>>>(p1_list, rd_n1, Tp, src, tpmin.p); note_launch();
+    if (rd_n2 > 0) { cache_scatter_kernel<<<blocks_for(rd_n2), 256, 0, st>>>(items2.p, rd_n2, Tp, src + rd_n1, tpmin.p); note_launch(); }
+    CUDA_TRY(cudaGetLastError());
+    rd_stage = 0;
+  }
+
+  void debug_lists(int64_t n1, int64_t n2) {
     const char* dbg_env = getenv("NNM_DEBUG");
     if (dbg_env && atoi(dbg_env) >= 2) {  // list statistics (expensive host copies)
       const int T = Tp;
@@ -3716,29 +3793,274 @@ __global__ void second_kernel(int n, const unsigned long long* b1l, const unsign
 }
 }  // namespace nnm
 
+namespace nnm {
+// ---- exchanges over peer memory (nnm_run_multi): every replica combines the partial
+// arrays of all replicas itself (P2P loads over NVLink / NVSwitch; same-device replicas
+// read local memory), so no broadcast step is needed.  Launched only after every
+// replica's producing step has completed (host join): no kernel waits on another.
+constexpr int MAX_REPLICAS = 16;
+struct PeerPtrs {
+  const void* p[MAX_REPLICAS];
+};
+
+__global__ void peer_min_u32_kernel(int64_t n, PeerPtrs in, int k, unsigned* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned v = 0xFFFFFFFFu;
+  for (int s = 0; s < k; ++s) v = min(v, static_cast<const unsigned*>(in.p[s])[i]);
+  out[i] = v;
+}
+
+__global__ void peer_max_u32_kernel(int64_t n, PeerPtrs in, int k, unsigned* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned v = 0u;
+  for (int s = 0; s < k; ++s) v = max(v, static_cast<const unsigned*>(in.p[s])[i]);
+  out[i] = v;
+}
+
+// g1 = min_s b1_s; g2 = min_s (b1_s == g1 ? b2_s : b1_s): the best and second-best keys of
+// the union of every replica's per-row top-2 (the second-smallest of distinct keys)
+__global__ void peer_keys_kernel(int64_t n, PeerPtrs b1, PeerPtrs b2, int k,
+                                 unsigned long long* __restrict__ g1,
+                                 unsigned long long* __restrict__ g2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long m1 = NONE_KEY;
+  for (int s = 0; s < k; ++s) m1 = min(m1, static_cast<const unsigned long long*>(b1.p[s])[i]);
+  unsigned long long m2 = NONE_KEY;
+  for (int s = 0; s < k; ++s) {
+    const unsigned long long a = static_cast<const unsigned long long*>(b1.p[s])[i];
+    m2 = min(m2, a == m1 ? static_cast<const unsigned long long*>(b2.p[s])[i] : a);
+  }
+  g1[i] = m1;
+  g2[i] = m2;
+}
+}  // namespace nnm
+
 extern "C" {
-int nnm_bv_cache(nnm_dataset* ds, int32_t synced, void** out_ptr, int64_t* out_count) {
+// ---- staged pruned round (multi-rank driver; DESIGN 6) --------------------------------
+static void staged_enter(nnm_dataset* ds) {
+  CUDA_TRY(cudaSetDevice(ds->device));
+  t_alloc_stream = ds->st;
+  CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
+}
+
+int nnm_bv_round_bound(nnm_dataset* ds, int32_t rank, int32_t world, uint32_t** out_caps,
+                       int64_t* out_count) {
   return guarded([&] {
-    if (!ds || !out_ptr || !out_count) invalid("null argument");
+    if (!ds || !out_caps || !out_count) invalid("null argument");
+    if (world < 1 || rank < 0 || rank >= world) invalid("bad rank / world");
     std::lock_guard<std::mutex> lk(ds->mu);
-    ds->tpmin_sync = ds->tpmin_on && synced != 0;
-    *out_ptr = ds->tpmin_on ? (void*)ds->tpmin.p : nullptr;
-    *out_count = ds->tpmin_on ? ds->tile_pairs() : 0;
+    staged_enter(ds);
+    ds->round_bound(ds->bv_metric, rank, world);
+    ds->sync();
+    *out_caps = ds->tc_cap_on ? reinterpret_cast<uint32_t*>(ds->ucap.p) : nullptr;
+    *out_count = ds->tc_cap_on ? ds->vn : 0;
   });
 }
 
-int nnm_bv_scan_pruned(nnm_dataset* ds, int32_t rank, int32_t world, uint64_t* B1_dev,
-                       uint64_t* B2_dev) {
+int nnm_bv_round_phase1(nnm_dataset* ds, int32_t rank, int32_t world, const uint32_t* caps_dev,
+                        uint64_t* B1_dev, uint64_t* B2_dev) {
   return guarded([&] {
     if (!ds || !B1_dev || !B2_dev) invalid("null argument");
     if (world < 1 || rank < 0 || rank >= world) invalid("bad rank / world");
     std::lock_guard<std::mutex> lk(ds->mu);
-    CUDA_TRY(cudaSetDevice(ds->device));
-    t_alloc_stream = ds->st;
-    CUDA_TRY(cudaDeviceSynchronize());  // caller buffers may be written on other streams
-    ds->pruned_scan_shard(ds->bv_metric, reinterpret_cast<unsigned long long*>(B1_dev),
-                          reinterpret_cast<unsigned long long*>(B2_dev), rank, world);
+    staged_enter(ds);
+    if (ds->tc_cap_on) ds->caps_read = caps_dev ? reinterpret_cast<const unsigned*>(caps_dev) : ds->ucap.p;
+    ds->round_phase1(reinterpret_cast<unsigned long long*>(B1_dev),
+                     reinterpret_cast<unsigned long long*>(B2_dev), rank, world);
     ds->sync();
+  });
+}
+
+int nnm_bv_round_phase2(nnm_dataset* ds, int32_t rank, int32_t world, const uint64_t* G1_dev,
+                        const uint64_t* G2_dev, uint64_t* B1_dev, uint64_t* B2_dev,
+                        uint32_t** out_cache, int64_t* out_count) {
+  return guarded([&] {
+    if (!ds || !G1_dev || !G2_dev || !B1_dev || !B2_dev || !out_cache || !out_count)
+      invalid("null argument");
+    if (world < 1 || rank < 0 || rank >= world) invalid("bad rank / world");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    staged_enter(ds);
+    ds->round_phase2(reinterpret_cast<const unsigned long long*>(G1_dev),
+                     reinterpret_cast<const unsigned long long*>(G2_dev),
+                     reinterpret_cast<unsigned long long*>(B1_dev),
+                     reinterpret_cast<unsigned long long*>(B2_dev), rank, world);
+    ds->sync();
+    const bool pend = ds->rd_stage == 3;
+    *out_cache = pend ? reinterpret_cast<uint32_t*>(ds->cachebuf.p) : nullptr;
+    *out_count = pend ? ds->rd_n1 + ds->rd_n2 : 0;
+  });
+}
+
+int nnm_bv_cache_scatter(nnm_dataset* ds) {
+  return guarded([&] {
+    if (!ds) invalid("null dataset");
+    std::lock_guard<std::mutex> lk(ds->mu);
+    staged_enter(ds);
+    ds->cache_scatter();
+    ds->sync();
+  });
+}
+
+// ---- single-process multi-GPU run: one replica per device (or several replicas on one
+// device, which runs the same exchange code sequentially), the staged pruned round on
+// 1/N shares with the exchanges done by peer kernels (DESIGN 6).  Without kl2/kl3/kl4 only;
+// the round path runs on replicas[0].
+}  // extern "C"
+namespace {
+template <class F>
+void par_replicas(nnm_dataset** reps, int k, F&& f) {
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(k);
+  for (int r = 0; r < k; ++r)
+    th.emplace_back([&, r] {
+      try {
+        CUDA_TRY(cudaSetDevice(reps[r]->device));
+        t_alloc_stream = reps[r]->st;
+        f(r, reps[r]);
+        reps[r]->sync();
+      } catch (...) {
+        err[r] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+}  // namespace
+extern "C" {
+
+int nnm_run_multi(nnm_dataset** reps, int32_t n_rep, int32_t metric, const nnm_constraints* cons,
+                  int64_t P, int32_t flags, nnm_merge* out_merges, int64_t* out_n_merges,
+                  int64_t* out_assign, int64_t* out_rounds, int32_t* out_stop,
+                  nnm_round_counters* out_counters, int64_t counters_cap, int64_t* out_n_counters,
+                  nnm_stats* stats) {
+  if (reps && n_rep == 1)
+    return nnm_run(reps[0], metric, cons, P, flags, out_merges, out_n_merges, out_assign, out_rounds,
+                   out_stop, out_counters, counters_cap, out_n_counters, stats);
+  return guarded([&] {
+    if (!reps || !cons || n_rep < 1) invalid("null argument");
+    if (n_rep > MAX_REPLICAS) invalid("at most " + std::to_string(MAX_REPLICAS) + " replicas");
+    for (int r = 0; r < n_rep; ++r) {
+      if (!reps[r]) invalid("null replica");
+      if (reps[r]->n != reps[0]->n || reps[r]->d != reps[0]->d) invalid("replicas differ in shape");
+      for (int q = 0; q < r; ++q)
+        if (reps[q] == reps[r]) invalid("a replica appears twice");
+    }
+    check_metric(metric);
+    check_constraints(cons);
+    if (P < 1) invalid("pairs_per_batch must be at least 1, got " + std::to_string(P));
+    const bool rounds_path = (flags & NNM_FLAG_ROUNDS) || cons->kl2 > 0 || cons->kl3 > 0 || cons->kl4 > 0;
+    if (rounds_path) {
+      const int rc = nnm_run(reps[0], metric, cons, P, flags, out_merges, out_n_merges, out_assign,
+                             out_rounds, out_stop, out_counters, counters_cap, out_n_counters, stats);
+      if (rc != NNM_OK) throw NnmError{rc, g_err};
+      return;
+    }
+    std::vector<nnm_dataset*> order(reps, reps + n_rep);
+    std::sort(order.begin(), order.end());
+    std::vector<std::unique_lock<std::mutex>> locks;
+    for (auto* d : order) locks.emplace_back(d->mu);
+    // peer access between the devices in use (no-op for same-device replicas)
+    for (int r = 0; r < n_rep; ++r)
+      for (int q = 0; q < n_rep; ++q) {
+        const int a = reps[r]->device, b = reps[q]->device;
+        if (a == b) continue;
+        int can = 0;
+        CUDA_TRY(cudaDeviceCanAccessPeer(&can, a, b));
+        if (!can) throw NnmError{NNM_E_UNSUPPORTED, "devices " + std::to_string(a) + " and " +
+                                                        std::to_string(b) + " have no peer access"};
+        CUDA_TRY(cudaSetDevice(a));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CUDA_TRY(e);
+        cudaGetLastError();
+      }
+    auto t0 = std::chrono::steady_clock::now();
+    const int64_t launches0 = g_launches.load();
+    nnm_dataset* ds0 = reps[0];
+    const int64_t n = ds0->n;
+    par_replicas(reps, n_rep, [&](int, nnm_dataset* ds) {
+      ds->stats = nnm_stats{};
+      ds->round_log.clear();
+      ds->pairs_covered = 0.0;
+      ds->stats.device = ds->device;
+      ds->stats.path = NNM_PATH_BORUVKA;
+      ds->bv_begin(metric, cons->dmax);
+      ds->G1.ensure(ds->vn);
+      ds->G2.ensure(ds->vn);
+      ds->ucapg.ensure(ds->vn);
+    });
+    ds0->stats.prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const int64_t vn = ds0->vn;
+    auto peers = [&](auto get) {
+      PeerPtrs pp{};
+      for (int q = 0; q < n_rep; ++q) pp.p[q] = get(reps[q]);
+      return pp;
+    };
+    const bool need = n > 1 && !(cons->kl1 > 0 && n <= cons->kl1);
+    while (need && ds0->bv_ncomp > 1) {
+      NvtxRange nv("nnm multi-replica round %lld", (long long)ds0->bv_round + 1);
+      const nnm_round_stat rl = ds0->rl_open(ds0->bv_round + 1);
+      par_replicas(reps, n_rep, [&](int r, nnm_dataset* ds) { ds->round_bound(metric, r, n_rep); });
+      if (ds0->tc_cap_on) {  // caps: min over the replicas' bound-pass shares
+        const PeerPtrs pc = peers([](nnm_dataset* q) { return (const void*)q->ucap.p; });
+        par_replicas(reps, n_rep, [&](int, nnm_dataset* ds) {
+          peer_min_u32_kernel<<<blocks_for(vn), 256, 0, ds->st>>>(vn, pc, n_rep, ds->ucapg.p); note_launch();
+          CUDA_TRY(cudaGetLastError());
+          ds->caps_read = ds->ucapg.p;
+        });
+      }
+      par_replicas(reps, n_rep, [&](int r, nnm_dataset* ds) { ds->round_phase1(ds->B1.p, ds->B2.p, r, n_rep); });
+      const PeerPtrs p1 = peers([](nnm_dataset* q) { return (const void*)q->B1.p; });
+      const PeerPtrs p2 = peers([](nnm_dataset* q) { return (const void*)q->B2.p; });
+      auto combine = [&](int, nnm_dataset* ds) {
+        peer_keys_kernel<<<blocks_for(vn), 256, 0, ds->st>>>(vn, p1, p2, n_rep, ds->G1.p, ds->G2.p); note_launch();
+        CUDA_TRY(cudaGetLastError());
+      };
+      par_replicas(reps, n_rep, combine);
+      par_replicas(reps, n_rep, [&](int r, nnm_dataset* ds) {
+        ds->round_phase2(ds->G1.p, ds->G2.p, ds->B1.p, ds->B2.p, r, n_rep);
+      });
+      par_replicas(reps, n_rep, combine);
+      if (ds0->rd_stage == 3) {  // tile-pair cache entries of this round: max over the replicas
+        const int64_t nc = ds0->rd_n1 + ds0->rd_n2;
+        const PeerPtrs pc = peers([](nnm_dataset* q) { return (const void*)q->cachebuf.p; });
+        par_replicas(reps, n_rep, [&](int, nnm_dataset* ds) {
+          ds->cacheg.ensure(nc);
+          peer_max_u32_kernel<<<blocks_for(nc), 256, 0, ds->st>>>(nc, pc, n_rep, ds->cacheg.p); note_launch();
+          CUDA_TRY(cudaGetLastError());
+        });
+        par_replicas(reps, n_rep, [&](int, nnm_dataset* ds) { ds->cache_scatter(ds->cacheg.p); });
+      }
+      std::vector<int64_t> added(n_rep);
+      par_replicas(reps, n_rep, [&](int r, nnm_dataset* ds) { added[r] = ds->bv_finish_round(ds->G1.p, ds->G2.p); });
+      for (int r = 1; r < n_rep; ++r)
+        if (added[r] != added[0]) throw NnmError{NNM_E_CUDA, "replicas diverged (internal error)"};
+      ds0->rl_close(rl, added[0]);
+      if (added[0] == 0) break;
+    }
+    auto tr0 = std::chrono::steady_clock::now();
+    CUDA_TRY(cudaSetDevice(ds0->device));
+    t_alloc_stream = ds0->st;
+    ds0->bv_end(cons->kl1, out_merges, out_n_merges, out_assign, out_rounds, out_stop);
+    ds0->stats.replay_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
+    nnm_stats agg = ds0->stats;
+    for (int r = 1; r < n_rep; ++r) {
+      agg.scans += reps[r]->stats.scans;
+      agg.pairs_evaluated += reps[r]->stats.pairs_evaluated;
+      agg.scan_ms = std::max(agg.scan_ms, reps[r]->stats.scan_ms);
+      agg.tc_items += reps[r]->stats.tc_items;
+      agg.ambiguous_rows = std::max(agg.ambiguous_rows, reps[r]->stats.ambiguous_rows);
+    }
+    agg.pairs_covered = ds0->pairs_covered;
+    agg.total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    agg.kernel_launches = g_launches.load() - launches0;
+    agg.replay_gpu_merges = ds0->stats.replay_gpu_merges;
+    ds0->stats = agg;
+    if (out_n_counters) *out_n_counters = 0;
+    if (stats) *stats = agg;
   });
 }
 

@@ -21,6 +21,7 @@ themselves through ``scheduler.run_round``.
 from __future__ import annotations
 
 import ctypes
+import os
 from collections.abc import Sequence
 from dataclasses import dataclass, field
 
@@ -33,7 +34,7 @@ from .pairgen import EligibilitySnapshot, TopPBuffer
 from .scheduler import PipelineConfig, UtilizationStats
 
 __all__ = ["RunConfig", "RunResult", "MergeLog", "order_batch", "process_batch", "run", "fit",
-           "run_arrays"]
+           "run_arrays", "run_arrays_multi", "replica_devices"]
 
 DEFAULT_PAIRS_PER_BATCH = 256
 
@@ -48,8 +49,11 @@ class RunConfig:
     blocks: int | None = None
     pipeline: PipelineConfig = PipelineConfig()
     exact_rounds: bool = False  # force the reference's round structure for every constraint set
+    n_gpus: int = 1  # replicas / GPUs of one process (nnm_run_multi); devices from NNM_DEVICES
 
     def __post_init__(self):
+        if self.n_gpus < 1:
+            raise ValidationError(f"n_gpus must be at least 1, got {self.n_gpus}")
         if self.pairs_per_batch < 1:
             raise ValidationError(
                 f"pairs_per_batch must be at least 1, got {self.pairs_per_batch}")
@@ -178,13 +182,74 @@ def run_arrays(ddata, constraints: ConstraintSet, P: int, metric: MetricKind,
             counters[: min(nc.value, ccap)], stats)
 
 
+def replica_devices(n_gpus: int) -> list:
+    """Devices of an n_gpus run: NNM_DEVICES (comma-separated, repeats allowed: several
+    replicas on one device run the same exchange code) or 0 .. n_gpus-1."""
+    env = os.environ.get("NNM_DEVICES")
+    if env:
+        devs = [int(x) for x in env.split(",") if x.strip()]
+        if len(devs) < n_gpus:
+            raise ValidationError(f"NNM_DEVICES lists {len(devs)} devices, n_gpus={n_gpus}")
+        return devs[:n_gpus]
+    return list(range(n_gpus))
+
+
+def run_arrays_multi(dds, constraints: ConstraintSet, P: int, metric: MetricKind,
+                     exact_rounds: bool = False):
+    """run_arrays over several resident replicas (nnm_run_multi)."""
+    if len(dds) == 1:
+        return run_arrays(dds[0], constraints, P, metric, exact_rounds)
+    n = dds[0].n
+    lib = _native.load()
+    merges = np.zeros(max(n - 1, 1), dtype=_native.MERGE_DTYPE)
+    assign = np.empty(n, np.int64)
+    ccap = n + 1
+    counters = np.zeros(ccap, dtype=_native.COUNTER_DTYPE)
+    nm, rounds, nc = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    stop = ctypes.c_int32()
+    st = _native.Stats()
+    cons = _native.Constraints(_opt(constraints.kl1), _opt(constraints.kl2),
+                               _opt(constraints.kl3), _opt(constraints.kl4),
+                               np.nan if constraints.dmax is None else float(constraints.dmax))
+    handles = (ctypes.c_void_p * len(dds))(*[d.handle for d in dds])
+    flags = _native.FLAG_ROUNDS if exact_rounds else 0
+    _native.check(lib.nnm_run_multi(handles, len(dds), metric_code(metric), ctypes.byref(cons),
+                                    int(P), flags, merges.ctypes.data, ctypes.byref(nm),
+                                    assign.ctypes.data, ctypes.byref(rounds), ctypes.byref(stop),
+                                    counters.ctypes.data, ccap, ctypes.byref(nc),
+                                    ctypes.byref(st)))
+    stats = st.as_dict()
+    stats["round_log"] = _native.round_log(dds[0].handle)
+    stats["replicas"] = [d.device for d in dds]
+    return (merges[: nm.value], assign, rounds.value, _native.STOP_NAMES[stop.value],
+            counters[: min(nc.value, ccap)], stats)
+
+
+def _replicas(dataset: Dataset, n_gpus: int) -> list:
+    devs = replica_devices(n_gpus)
+    cache = getattr(dataset, "_replica_cache", None)
+    if cache is not None and cache[0] == tuple(devs):
+        return cache[1]
+    first = _native.device_dataset(dataset)
+    reps = [first if first.device == devs[0] else _native.DeviceDataset(dataset.values, device=devs[0])]
+    reps += [_native.DeviceDataset(dataset.values, device=dv) for dv in devs[1:]]
+    object.__setattr__(dataset, "_replica_cache", (tuple(devs), reps))
+    return reps
+
+
 def run(dataset: Dataset, config: RunConfig) -> RunResult:
-    """Cluster to completion on the GPU (engine.py:154-199)."""
+    """Cluster to completion on the GPU (engine.py:154-199); config.n_gpus > 1 runs the
+    Boruvka path over that many GPU replicas in this process (nnm_run_multi)."""
     if not isinstance(dataset, Dataset):
         dataset = Dataset(values=np.asarray(dataset))
-    dd = _native.device_dataset(dataset)
-    merges, assign, rounds, stop, counters, dstats = run_arrays(
-        dd, config.constraints, config.pairs_per_batch, config.metric, config.exact_rounds)
+    if config.n_gpus > 1:
+        merges, assign, rounds, stop, counters, dstats = run_arrays_multi(
+            _replicas(dataset, config.n_gpus), config.constraints, config.pairs_per_batch,
+            config.metric, config.exact_rounds)
+    else:
+        dd = _native.device_dataset(dataset)
+        merges, assign, rounds, stop, counters, dstats = run_arrays(
+            dd, config.constraints, config.pairs_per_batch, config.metric, config.exact_rounds)
     wall = dstats["total_ms"] / 1e3
     stats = UtilizationStats(worker_busy={"gpu0": dstats["scan_ms"] / 1e3},
                              worker_idle={"gpu0": max(0.0, wall - dstats["scan_ms"] / 1e3)},
@@ -195,9 +260,11 @@ def run(dataset: Dataset, config: RunConfig) -> RunResult:
 
 
 def fit(X, *, metric="euclidean", kl1=None, kl2=None, kl3=None, kl4=None, dmax=None,
-        pairs_per_batch: int = DEFAULT_PAIRS_PER_BATCH, exact_rounds: bool = False) -> RunResult:
+        pairs_per_batch: int = DEFAULT_PAIRS_PER_BATCH, exact_rounds: bool = False,
+        n_gpus: int = 1) -> RunResult:
     """Convenience entry: fit on an (n, d) float array with the paper's constraints."""
     kind = MetricKind.parse(metric) if isinstance(metric, str) else metric
     cfg = RunConfig(constraints=ConstraintSet(kl1=kl1, kl2=kl2, kl3=kl3, kl4=kl4, dmax=dmax),
-                    pairs_per_batch=pairs_per_batch, metric=kind, exact_rounds=exact_rounds)
+                    pairs_per_batch=pairs_per_batch, metric=kind, exact_rounds=exact_rounds,
+                    n_gpus=n_gpus)
     return run(Dataset(values=np.asarray(X, dtype=np.float64)), cfg)

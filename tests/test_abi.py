@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_symbols():
         assert hasattr(lib, name), name
     lib.nnm_abi_version.restype = ctypes.c_int
-    assert lib.nnm_abi_version() == 3
+    assert lib.nnm_abi_version() == 4
 
 
 def test_no_cpu_fallback_without_device():

@@ -1,11 +1,14 @@
-"""Functional test of the multi-GPU driver on the real kernels (@gpu).
+"""Functional test of the multi-process driver on the real kernels (@gpu).
 
-Two processes (torch.distributed, gloo) both drive device 0 through
-paper_1402_3789_b200.distributed.run_boruvka_distributed: each rank runs the
-pruned scan on its phase-2 share (nnm_bv_scan_pruned), the keys are combined with
-two all-reduce(MIN), and every rank finishes the rounds identically.  The merge log
-and labels must equal the single-process run byte for byte, on both ranks.  This
-checks correctness of the sharded path only (the ranks share one GPU; no timing).
+Processes (torch.distributed, gloo) all drive device 0 through
+paper_1402_3789_b200.distributed.run_boruvka_distributed: each rank runs the staged
+pruned round on its shares (nnm_bv_round_bound / _phase1 / _phase2), the caps, keys
+and this round's tile-pair cache entries are combined with all-reduces, and every rank
+finishes the rounds identically.  The merge log and labels must equal the
+single-process run byte for byte on every rank, and the ranks' evaluated pairs must add
+up to the single run's (every item scanned by exactly one rank).  The ranks share one
+GPU and only the host orchestrates the exchanges (no kernel waits on another); this
+checks correctness of the sharded path, not timing.
 """
 
 from __future__ import annotations
@@ -41,8 +44,9 @@ def _worker(rank, world, port, X, kwargs, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("kwargs", [{}, {"dmax": 4.0}, {"metric": "manhattan"}])
-def test_two_rank_pruned_run_equals_single(kwargs):
+def test_multi_rank_pruned_run_equals_single(kwargs, world):
     import torch.multiprocessing as mp
 
     import paper_1402_3789_b200 as nnm
@@ -54,7 +58,7 @@ def test_two_rank_pruned_run_equals_single(kwargs):
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, X, kwargs, out)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, X, kwargs, out)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -62,8 +66,34 @@ def test_two_rank_pruned_run_equals_single(kwargs):
         assert p.exitcode == 0
     want_m = single.merges.array.tobytes()
     want_a = single.assignments.tobytes()
-    for r in range(2):
+    for r in range(world):
         m, a, rounds, stop, _ = out[r]
         assert m == want_m, r
         assert a == want_a, r
         assert stop == single.stop_reason
+    # every phase-1 / phase-2 item was scanned by exactly one rank
+    assert sum(out[r][4] for r in range(world)) == single.device_stats["pairs_evaluated"]
+
+
+def test_tile_pair_cache_on_off_identical():
+    """The tile-pair bound cache only prunes: NNM_TPCACHE=0 gives the same merge log and
+    labels, and evaluates at least as many pairs."""
+    import subprocess
+    import sys
+
+    from nnm_testutil import ROOT
+
+    code = ("import hashlib, numpy as np, paper_1402_3789_b200 as nnm\n"
+            "X = nnm.generate_synthetic(20000, 25, 60, 1.0, seed=8)[0]\n"
+            "r = nnm.fit(X)\n"
+            "print(hashlib.sha256(r.merges.array.tobytes() + r.assignments.tobytes()).hexdigest(),"
+            " r.device_stats['pairs_evaluated'])\n")
+    outs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, NNM_TPCACHE=flag)
+        p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(p.stdout.split())
+    assert outs[0][0] == outs[1][0]
+    assert float(outs[1][1]) >= float(outs[0][1])

@@ -144,10 +144,9 @@ def test_boruvka_vs_oracle_flat(nnm, metric, kind):
         assert np.array_equal(res.assignments, a_or), cons
 
 
-@pytest.mark.parametrize("pruned", [False, True])
-def test_staged_multi_range_equals_single(nnm, pruned):
-    """Emulate R ranks on one GPU: disjoint tile-pair shares (dense ranges, or the
-    pruned scan's phase-2 shares) + min-combine of keys."""
+def test_staged_dense_ranges_equal_single(nnm):
+    """Emulate 3 ranks on one GPU with the dense staged scan (nnm_bv_scan): disjoint
+    tile-pair ranges + the min-combine of keys give the single-GPU merge log."""
     import ctypes
 
     from paper_1402_3789_b200 import _native
@@ -169,11 +168,7 @@ def test_staged_multi_range_equals_single(nnm, pruned):
             lo, hi = shard_range(tp.value, r, R)
             b1 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
             b2 = torch.empty(rows.value, dtype=torch.int64, device="cuda")
-            if pruned:
-                _native.check(lib.nnm_bv_scan_pruned(dd.handle, r, R, b1.data_ptr(),
-                                                     b2.data_ptr()))
-            else:
-                _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
+            _native.check(lib.nnm_bv_scan(dd.handle, lo, hi, b1.data_ptr(), b2.data_ptr()))
             parts.append((b1, b2))
         torch.cuda.synchronize()
         g1 = torch.stack([p[0] for p in parts]).min(0).values
@@ -199,6 +194,26 @@ def test_staged_multi_range_equals_single(nnm, pruned):
     for f in FIELDS + ("round",):
         assert np.array_equal(merges[: nm.value][f], want.merges.array[f]), f
     assert np.array_equal(assign, want.assignments)
+
+
+@pytest.mark.parametrize("replicas", [2, 3, 4])
+@pytest.mark.parametrize("kw", [{}, {"dmax": 4.0}, {"metric": "manhattan"}, {"kl1": 9}])
+def test_multi_replica_run_equals_single(nnm, replicas, kw, monkeypatch):
+    """RunConfig(n_gpus=R) through nnm_run_multi with R replicas on device 0 (NNM_DEVICES):
+    sharded bound / phase-1 / phase-2 scans, caps / keys / cache combined by the peer
+    kernels -- byte-identical to one replica, and the replicas together evaluate exactly
+    the single run's pairs (each item scanned once)."""
+    X = nnm.generate_synthetic(9000, 25, 30, 1.0, seed=41)[0]
+    X = X[np.random.default_rng(6).permutation(len(X))]
+    single = nnm.fit(X, **kw)
+    monkeypatch.setenv("NNM_DEVICES", ",".join(["0"] * replicas))
+    multi = nnm.fit(X, n_gpus=replicas, **kw)
+    for f in FIELDS + ("round",):
+        assert np.array_equal(multi.merges.array[f], single.merges.array[f]), f
+    assert np.array_equal(multi.assignments, single.assignments)
+    assert multi.stop_reason == single.stop_reason
+    assert multi.device_stats["replicas"] == [0] * replicas
+    assert multi.device_stats["pairs_evaluated"] == single.device_stats["pairs_evaluated"]
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 127, 129, 300, 2049])
