@@ -79,6 +79,8 @@ struct TcSmem {
   int ringrt[TC_RING];                 // row-tile index of item q, negated-minus-one when item q
                                        // is the first of its row tile (producer)
   int slot[2][8];
+  int nslot[2];                        // distinct components of the row tile (select_slots)
+  int chk[TC_STAGES];                  // item may hold unmasked same-component pairs (prep)
   unsigned lbw[TC_EPI_GROUPS][2][4];   // tile-pair bound: per-quadrant minima of an item
   int lbcnt[TC_EPI_GROUPS][2];         // (epilogue group, item parity) arrivals
   unsigned long long full[TC_STAGES], prepped[TC_STAGES], empty[TC_STAGES];
@@ -317,7 +319,7 @@ __device__ __forceinline__ void load_row(const float* tile, int r, int d, float 
 // Mask slots of a row tile: the first kc distinct components in position order
 // (parallel first-occurrence test + warp ballots).  Called by one prep warp: lane l owns
 // rows l, l + 32, l + 64, l + 96 (one 32-row block per ballot, in position order).
-__device__ __forceinline__ void select_slots(const int* comp, int* slot, int lane, int kc) {
+__device__ __forceinline__ void select_slots(const int* comp, int* slot, int* nslot, int lane, int kc) {
   int c[4];
   bool f[4];
 #pragma unroll
@@ -341,6 +343,7 @@ __device__ __forceinline__ void select_slots(const int* comp, int* slot, int lan
     base += __popc(m);
   }
   if (lane < 8 && lane >= min(base, kc)) slot[lane] = -2;
+  if (lane == 0) *nslot = base;
   __syncwarp();
 }
 
@@ -480,7 +483,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         if (opens) {
           // first item of the row tile: this group prepares the A operand
           mbar_wait(&S.afull[xb], (rt >> 1) & 1);
-          select_slots(S.acomp[xb], S.slot[xb], pt, kc);
+          select_slots(S.acomp[xb], S.slot[xb], &S.nslot[xb], pt, kc);
 #pragma unroll
           for (int k = 0; k < 8; ++k) slot[k] = S.slot[xb][k];
 #pragma unroll
@@ -538,7 +541,18 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         }
         write_tail(S.B[s], col, d, kc, hi, lo, slot_hits(cj, slot), 1.f);
       }
-      if (pt == 0) trace(p, 5, q, 1);
+      if (pt == 0) {
+        trace(p, 5, q, 1);
+        // unmasked same-component pairs are possible only if the row tile has more
+        // components than slots and the two tiles' component ranges overlap
+        const int Jt = S.ring[q % TC_RING].y;
+        bool chk = S.nslot[xb] > kc;
+        if (chk && p.trange) {
+          const int2 a = __ldg(p.trange + I), b = __ldg(p.trange + Jt);
+          chk = !(b.y < a.x || a.y < b.x);
+        }
+        S.chk[s] = chk ? 1 : 0;
+      }
       if (!(p.dbg & 4)) fence_proxy_async();  // (dbg 4: timing experiment only)
       if (pt == 0) trace(p, 7, q, 0);
       __syncwarp();
@@ -644,9 +658,14 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
           // real eligible-or-farther partner with S <= (sqrt(v + E) + eta)^2: the row's
           // rigorous upper bound, min over the row tile's items, atomicMin into its
           // component's cap at the end of the row tile (flush_row)
-          float b1 = -INFINITY;
+          // every same-component pair is masked by the slots (or none exists): the row
+          // maximum over all columns is over valid cross-component columns (pads sit at
+          // -2^60 and cannot win while the tile holds a real point)
+          const bool chk = S.chk[s] != 0;
+          float b1 = chk ? -INFINITY : rmax;
 #pragma unroll 1
           for (int gidx = 0; gidx < TILE / 8; ++gidx) {
+            if (!chk) break;
             if (!__any_sync(0xFFFFFFFFu, ci >= 0 && gmax[gidx] > b1)) continue;
             float w[8];
             tmem_ld8(lane_base + a * TILE + gidx * 8, w);

@@ -39,6 +39,7 @@ struct TcArgs {
   // otherwise every row threshold is capped by its component's value (nullptr: off)
   unsigned* ucap;
   int bound_only;
+  const int2* trange;     // [T] min / max component label per tile (nullptr: always check)
 };
 
 size_t tc_smem_bytes();

@@ -27,6 +27,7 @@ large P to finish in few rounds):
   c5msub C4 X[::10] manhattan, full dendrogram
   c5csub C4 X[::10] chebyshev, full dendrogram
   c2     C2 100k x 25, kl1=400 kl2=300 kl3=450 kl4=150, P=256 (rounds + counters)
+  c2nokl4  C2's X with kl1=400 kl2=300 kl3=450 (no kl4; merge list P-invariant, P=4096)
   c4top  C4 2M x 25 round-1 global_top_p with P=256 (singleton snapshot)
 """
 
@@ -78,6 +79,9 @@ RUNS = {
     "c5csub": dict(config="c4", stride=SUB_STRIDE, metric="chebyshev", cons={}, P=1 << 18),
     "c2": dict(config="c2", stride=1, metric="euclidean",
                cons=dict(kl1=400, kl2=300, kl3=450, kl4=150), P=256),
+    # kl2/kl3 without kl4: P-invariant merge list (F3), so the oracle takes P = 4096
+    "c2nokl4": dict(config="c2", stride=1, metric="euclidean",
+                    cons=dict(kl1=400, kl2=300, kl3=450), P=4096),
 }
 
 

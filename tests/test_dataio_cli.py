@@ -123,8 +123,9 @@ def test_cli_generate_round_trips(tmp_path):
 @pytest.mark.parametrize("exact_rounds", [True, False])
 def test_cli_cluster_matches_reference_bytes(golden, tmp_path, exact_rounds):
     """GPU CLI vs the reference CLI on the same input and flags.  With --exact-rounds
-    every byte of assignments.csv / merges.csv matches; on the default Boruvka path
-    (no kl2/kl3/kl4) everything but the P-dependent round column matches."""
+    every byte of assignments.csv / merges.csv matches (also with kl4); otherwise (the
+    Boruvka path, or kl2/kl3 in large batches) everything but the P-dependent round column
+    matches."""
     from paper_1402_3789_b200.cli import main
 
     for name, case in golden["runs"].items():
@@ -140,7 +141,9 @@ def test_cli_cluster_matches_reference_bytes(golden, tmp_path, exact_rounds):
         assert (od / "assignments.csv").read_text() == case["assignments"], name
         got = (od / "merges.csv").read_text()
         st = json.load(open(od / "stats.json"))
-        round_path = exact_rounds or any(f in case["flags"] for f in ("--kl2", "--kl3", "--kl4"))
+        # rounds (and the per-round skip counters) are part of the result only with kl4
+        # or --exact-rounds; kl2/kl3 alone run large GPU batches
+        round_path = exact_rounds or "--kl4" in case["flags"]
         if round_path:
             assert got == case["merges"], name
             for k, v in case["stats"].items():

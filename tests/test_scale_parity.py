@@ -128,6 +128,20 @@ def test_c2_full_run_vs_oracle(nnm):
     assert rc == g["counters"]
 
 
+def test_c2_without_kl4_fast_path_vs_oracle(nnm):
+    """C2's data with kl1/kl2/kl3 and no kl4: the GPU's large-batch rounds reproduce the
+    oracle's merge list (P-invariant without kl4) with >= 10x fewer rounds
+    than the reference's round structure at P=256 (exact_rounds)."""
+    from paper_1402_3789_b200.datagen import config_dataset
+
+    g = _golden("c2nokl4")
+    X = config_dataset("c2")
+    res = nnm.fit(X, pairs_per_batch=256, **g["constraints"])
+    _check(res, g)
+    ref_rounds = nnm.fit(X, pairs_per_batch=256, exact_rounds=True, **g["constraints"]).rounds
+    assert res.rounds * 10 <= ref_rounds, (res.rounds, ref_rounds)
+
+
 def test_c4_round1_top256_vs_oracle(nnm, c4):
     from paper_1402_3789_b200.metrics import MetricKind
     from paper_1402_3789_b200.pairgen import EligibilitySnapshot, gpu_top_p
