@@ -1320,6 +1320,56 @@ __global__ void cache_scatter_kernel(const int2* __restrict__ items, int64_t cnt
   tpmin[tri_index(T, min(it.x, it.y), max(it.x, it.y))] = in[t];
 }
 
+// Phase-2 enumeration from the tile-pair bound table, appending the kept tile pairs as
+// u64 keys (I << 32 | J) with warp-aggregated atomics (unordered; sorted afterwards so
+// that every rank derives the identical list).  Same keep rule as enum_table_kernel.
+__global__ void enum_append_kernel(const unsigned* __restrict__ bnd, const int2* __restrict__ trange,
+                                   const double* __restrict__ umax, const unsigned* __restrict__ bits,
+                                   int T, unsigned long long* __restrict__ out,
+                                   unsigned long long* __restrict__ count, unsigned long long cap) {
+  const int I = blockIdx.x;
+  const int64_t w0 = tri_index(T, I, I);
+  const int2 tI = trange[I];
+  const double uI = umax[I];
+  const int lane = threadIdx.x & 31;
+  for (int J0 = I; J0 < T; J0 += blockDim.x) {
+    const int J = J0 + threadIdx.x;
+    bool k = false;
+    if (J < T) {
+      const int64_t w = w0 + (J - I);
+      const int2 tJ = trange[J];
+      k = !((bits[w >> 5] >> (w & 31)) & 1u) &&
+          !(tI.x == tI.y && tJ.x == tJ.y && tI.x == tJ.x);  // same_single(I, J)
+      if (k && J != I) k = !((double)__uint_as_float(bnd[w]) > fmax(uI, umax[J]));
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, k);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (k) {
+      const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
+      if (at < cap) out[at] = ((unsigned long long)I << 32) | (unsigned)J;
+    }
+  }
+}
+
+// sorted u64 item keys (I << 32 | J) -> int2 (I, J)
+__global__ void keys_to_items_kernel(const unsigned long long* __restrict__ keys, int64_t n,
+                                     int2* __restrict__ items) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) items[t] = make_int2((int)(keys[t] >> 32), (int)(keys[t] & 0xFFFFFFFFull));
+}
+
+// int2 (I <= J, or (-1, -1) padding) -> u64 key (padding ~0: sorts last)
+__global__ void items_to_keys_kernel(const int2* __restrict__ items, int64_t n,
+                                     unsigned long long* __restrict__ keys) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int2 it = items[t];
+  keys[t] = it.x < 0 ? ~0ull : (((unsigned long long)it.x << 32) | (unsigned)it.y);
+}
+
 __global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt,
                                   const int* __restrict__ tcount, unsigned long long* acc) {
   // real point pairs covered by a list of tile pairs (for the stats)
@@ -2168,6 +2218,13 @@ struct nnm_dataset {
     const int64_t n_up = w_end - w_begin;
     if (n_up <= 0) return;
     tc_prepare();
+    // the bound pass and the exact pass of phase 1 scan the same list: mirror + sort once
+    const bool reuse = !umax && tc_list_epoch == scan_epoch && tc_list_items == items &&
+                       tc_list_wb == w_begin && tc_list_we == w_end;
+    if (reuse) {
+      tc_launch(b1, b2, thr_hi, items, w_begin, w_end, tc_list_nfull);
+      return;
+    }
     tc_items.ensure((size_t)2 * n_up);
     counters.ensure(8);
     CUDA_TRY(cudaMemsetAsync(counters.p + 5, 0, sizeof(unsigned long long), st));
@@ -2182,9 +2239,25 @@ struct nnm_dataset {
     CUDA_TRY(cudaGetLastError());
     thrust::sort_by_key(thrust::cuda::par(talloc).on(st), tc_keys.p, tc_keys.p + 2 * n_up, tc_js.p);
     const int64_t nfull = 2 * n_up - (int64_t)read1(counters.p + 5);
+    tc_list_epoch = scan_epoch;
+    tc_list_items = items;
+    tc_list_wb = w_begin;
+    tc_list_we = umax ? -1 : w_end;  // lists with orientation drops are not reused
+    tc_list_nfull = nfull;
     if (nfull <= 0) return;
     tc_items_kernel<<<blocks_for(nfull), 256, 0, st>>>(tc_keys.p, tc_js.p, nfull, tc_items.p); note_launch();
     CUDA_TRY(cudaGetLastError());
+    tc_launch(b1, b2, thr_hi, items, w_begin, w_end, nfull);
+  }
+
+  int64_t scan_epoch = 0;  // bumped every round: the mirrored list is reused within a round
+  int64_t tc_list_epoch = -1, tc_list_wb = -1, tc_list_we = -1, tc_list_nfull = 0;
+  const int2* tc_list_items = nullptr;
+
+  void tc_launch(unsigned long long* b1, unsigned long long* b2, float thr_hi, const int2* items,
+                 int64_t w_begin, int64_t w_end, int64_t nfull) {
+    const int64_t n_up = w_end - w_begin;
+    if (nfull <= 0) return;
     TcArgs a;
     a.img = tc_img.p;
     a.tnorm = tc_tnorm.p;
@@ -2566,6 +2639,40 @@ struct nnm_dataset {
     build_tile_tables(kind);
   }
 
+  DevBuf<unsigned long long> ekeys, ekeys2;  // item keys (I << 32 | J) and sort scratch
+  DevBuf<char> sort_tmp;
+
+  int item_bits() const {
+    int b = 1;
+    while (b < 31 && ((int64_t)1 << b) < Tp) ++b;
+    return b;
+  }
+
+  // in-place ascending radix sort of u64 keys over bits [0, 32 + bits) of the high word
+  // (keys = hi << 32 | lo with hi < 2^bits_hi, or ~0 padding when all 64 bits are sorted)
+  void sort_keys(unsigned long long* keys, int64_t n, int hi_bits) {
+    if (n <= 1) return;
+    ekeys2.ensure(n);
+    const int end_bit = std::min(64, 32 + hi_bits);
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, ekeys2.p, (int)n, 0, end_bit, st));
+    sort_tmp.ensure(std::max<size_t>(tb, 1));
+    CUDA_TRY(cub::DeviceRadixSort::SortKeys(sort_tmp.p, tb, keys, ekeys2.p, (int)n, 0, end_bit, st));
+    CUDA_TRY(cudaMemcpyAsync(keys, ekeys2.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+  }
+
+  // (I, J) items with (-1, -1) padding -> sorted unique items at the front; returns the count
+  int64_t sort_unique_items(int2* items, int64_t n) {
+    ekeys.ensure(n);
+    items_to_keys_kernel<<<blocks_for(n), 256, 0, st>>>(items, n, ekeys.p); note_launch();
+    sort_keys(ekeys.p, n, 32);  // all 64 bits: the ~0 padding must sort last
+    auto* end = thrust::unique(thrust::cuda::par(talloc).on(st), ekeys.p, ekeys.p + n);
+    int64_t m = end - ekeys.p;
+    if (m > 0 && read1(ekeys.p + (m - 1)) == ~0ull) --m;
+    if (m > 0) { keys_to_items_kernel<<<blocks_for(m), 256, 0, st>>>(ekeys.p, m, items); note_launch(); }
+    return m;
+  }
+
   bool glb_ready() const { return glb_metric >= 0 && glb_metric == geom_metric; }
   bool nbr_ready() const { return nbr_metric >= 0 && nbr_metric == geom_metric; }
 
@@ -2643,16 +2750,9 @@ struct nnm_dataset {
       phase1_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
     }
     CUDA_TRY(cudaGetLastError());
-    auto* k64 = reinterpret_cast<unsigned long long*>(items1.p);  // (I, J) -> J << 32 | I order
-    // sort by (I, J): int2 memory is {x=I, y=J}; as u64 little-endian = J << 32 | I -> swap to key
-    thrust::sort(thrust::cuda::par(talloc).on(st), k64, k64 + (size_t)Tp * PK, ItemLess());
-    auto* end = thrust::unique(thrust::cuda::par(talloc).on(st), k64, k64 + (size_t)Tp * PK);
-    n1 = end - k64;
-    // drop the (-1,-1) padding, which sorts first
-    int2 first = read1(items1.p);
-    int64_t skip = (first.x < 0) ? 1 : 0;
-    n1 -= skip;
-    int2* list1 = items1.p + skip;
+    // sort by (I, J) as u64 keys (padding sorts last), drop duplicates and the padding
+    n1 = sort_unique_items(items1.p, (int64_t)Tp * PK);
+    int2* list1 = items1.p;
     pbits.ensure((size_t)(W + 31) / 32);
     CUDA_TRY(cudaMemsetAsync(pbits.p, 0, ((W + 31) / 32) * sizeof(unsigned), st));
     if (n1 > 0) { mark_items_kernel<<<blocks_for(n1), 256, 0, st>>>(list1, n1, Tp, pbits.p); note_launch(); }
@@ -2666,14 +2766,35 @@ struct nnm_dataset {
     const int64_t W = tile_pairs();
     tumax.ensure(Tp);
     tile_umax_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, ucomp.p, bv_thr, tumax.p); note_launch();
+    if (glb_ready()) {  // stream the bound table, append kept pairs, sort the (small) list
+      counters.ensure(8);
+      unsigned long long cap = std::max<unsigned long long>(ekeys.n, 1u << 20);
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        ekeys.ensure(cap);
+        CUDA_TRY(cudaMemsetAsync(counters.p + 4, 0, sizeof(unsigned long long), st));
+        enum_append_kernel<<<Tp, 256, 0, st>>>(tpmin_use ? tpmin.p : glb.p, tile_range.p, tumax.p,
+                                               pbits.p, Tp, ekeys.p, counters.p + 4, ekeys.n);
+        note_launch();
+        CUDA_TRY(cudaGetLastError());
+        const unsigned long long cnt = read1(counters.p + 4);
+        if (cnt <= ekeys.n) {
+          n2 = (int64_t)cnt;
+          break;
+        }
+        cap = cnt + cnt / 4;
+        if (attempt == 1) throw NnmError{NNM_E_CUDA, "phase-2 list overflow after resize"};
+      }
+      items2.ensure(std::max<int64_t>(n2, 1));
+      if (n2 > 0) {
+        sort_keys(ekeys.p, n2, item_bits());
+        keys_to_items_kernel<<<blocks_for(n2), 256, 0, st>>>(ekeys.p, n2, items2.p); note_launch();
+      }
+      return;
+    }
     pkeep.ensure(W);
     pcount.ensure(Tp);
     poffset.ensure(Tp + 1);
-    if (glb_ready())
-      enum_table_kernel<<<Tp, 256, 0, st>>>(tpmin_use ? tpmin.p : glb.p, tile_range.p, tumax.p,
-                                            pbits.p, Tp, pkeep.p, pcount.p);
-    else
-      enum_count_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
+    enum_count_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tcn32.p, tr32.p, tile_range.p, tumax.p, pbits.p,
                                                Tp, d, tpmin_use ? tpmin.p : nullptr,
                                                pkeep.p, pcount.p);
     note_launch();
@@ -2729,6 +2850,7 @@ struct nnm_dataset {
       throw NnmError{NNM_E_INVALID, "staged round: the tile-pair cache of the previous round was "
                                     "not exchanged (nnm_bv_cache_scatter)"};
     ensure_geometry(metric);
+    ++scan_epoch;
     tpmin_use = tpmin_on;  // exchanged every round (compact MAX), so consistent on all ranks
     tile_range.ensure(Tp);
     tile_range_kernel<<<Tp, TILE, 0, st>>>(comp.p, vn, Tp, tile_range.p); note_launch();
