@@ -91,7 +91,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._pump, daemon=True)
             self.thread.start()
@@ -249,15 +249,15 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def _load_traffic(name: str):
-    """DRAM bytes per unit of the scan kernel from a committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", name)
-    if os.path.exists(p):
-        try:
-            return json.load(open(p))
-        except (OSError, ValueError):
-            return None
-    return None
+def _load_traffic(cfg: str):
+    """DRAM bytes per launch of the config's dominant scan kernel, from the committed ncu
+    launch list of one device step of that config (profiles/r2_traffic.json, written by
+    tools/traffic_from_launches.py)."""
+    p = os.path.join(ROOT, "profiles", "r2_traffic.json")
+    try:
+        return json.load(open(p)).get(cfg)
+    except (OSError, ValueError):
+        return None
 
 
 def _measured_peaks() -> dict:
@@ -415,16 +415,16 @@ def run_gpu(args) -> None:
         mp = _measured_peaks()
         bf16 = mp.get("bf16_tflops_sustained") or mp.get("bf16_tflops")
         tf32_peak = (bf16 / 2.0) if bf16 else 1100.0
-        tr = _load_traffic("tc_scan_traffic.json")
+        tr = _load_traffic(args.config)
         mma_tflops = tc_items * 2.0 * 128 * 128 * 32 / (scan_ms / 1e3) / 1e12
         roofline = {
             "bound": "tensor", "achieved": alg_tflops, "peak": tf32_peak, "unit": "TFLOP/s",
             "frac": alg_tflops / tf32_peak,
-            "traffic": (tr.get("dram_bytes_per_launch") or
-                        tr["dram_bytes_per_item"] * tc_items / max(scans, 1)) if tr else None,
-            "traffic_note": "ncu dram__bytes_read+write of one captured launch (round-2 phase-1 "
-                            "seed scan, profiles/tc_scan_traffic.json); the FP64 exact-key gathers "
-                            "(X64 rows) dominate it",
+            "traffic": tr["dram_bytes_per_launch"] if tr else None,
+            "traffic_note": ("ncu dram__bytes_read+write per launch of this kernel, averaged over "
+                             f"the {tr['launches']} launches of one {args.config} device step "
+                             "(profiles/r2_traffic.json); bound passes, exact passes and FP64 "
+                             "exact-key gathers of X64 rows included") if tr else None,
             "kernel": "tc_scan_kernel (tcgen05 kind::tf32 128x128x32 MMA per tile pair, TMEM "
                       "accumulators; fused centring, component masks, threshold filter, exact-key "
                       "top-2)",
@@ -437,15 +437,17 @@ def run_gpu(args) -> None:
             "avg_launch_ms": avg_launch_ms, "launches": scans, "tc_items": tc_items,
             "scan_share_of_step": scan_ms / (ms_dev * args.steps)}
     else:
-        tr = _load_traffic("scan_traffic.json")
-        bpp = tr.get("dram_bytes_per_pair") if tr else None
+        tr = _load_traffic(args.config)
+        kname = tr["kernel"] if tr else "scan_reg_kernel"
         roofline = {"bound": "fp32", "achieved": alg_tflops, "peak": peak.value, "unit": "TFLOP/s",
                     "frac": alg_tflops / peak.value if peak.value else None,
-                    "traffic": (bpp * pairs_eval / max(scans, 1)) if bpp is not None else None,
-                    "traffic_note": "dram bytes per launch = ncu dram__bytes_read+write per pair "
-                                    "(profiles/scan_traffic.json) x average pairs per launch",
-                    "kernel": "scan_reg_kernel (fused FP32 dot-form distance + eligibility + per-row "
-                              "top-2 threshold filter)",
+                    "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                    "traffic_note": ("ncu dram__bytes_read+write per launch of this kernel, "
+                                     f"averaged over the {tr['launches']} launches of one "
+                                     f"{args.config} device step (profiles/r2_traffic.json)")
+                                    if tr else None,
+                    "kernel": f"{kname} (fused FP32 distance + eligibility (components, dmax, "
+                              "kl2/kl3 sizes) + per-row top-1/top-2 threshold filter)",
                     "peak_source": "measured FFMA2 microbenchmark on this GPU (MEASURED_PEAKS.json "
                                    "has no FP32 entry)",
                     "avg_launch_ms": avg_launch_ms, "launches": scans,
