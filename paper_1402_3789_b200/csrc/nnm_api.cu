@@ -1370,6 +1370,14 @@ __global__ void items_to_keys_kernel(const int2* __restrict__ items, int64_t n,
   keys[t] = it.x < 0 ? ~0ull : (((unsigned long long)it.x << 32) | (unsigned)it.y);
 }
 
+__global__ void pos_caps_kernel(int64_t n, const int* __restrict__ comp,
+                                const unsigned* __restrict__ caps, unsigned* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = comp[i];
+  out[i] = c >= 0 ? caps[c] : 0x7f800000u;
+}
+
 __global__ void item_pairs_kernel(const int2* __restrict__ items, int64_t cnt,
                                   const int* __restrict__ tcount, unsigned long long* acc) {
   // real point pairs covered by a list of tile pairs (for the stats)
@@ -1984,6 +1992,20 @@ struct nnm_dataset {
   DevBuf<unsigned> tpmin;
   // component caps (TC scan): bound pass over the phase-1 items, then capped exact scans
   DevBuf<unsigned> ucap;        // this rank's caps from its bound-pass share (u32 fp32 bits)
+  DevBuf<unsigned> capp;        // per position: its component's cap (staged by the scan)
+  DevBuf<int> tc_slots;         // [Tp][16] per-round slot records (tc_tails)
+  int64_t tc_tails_epoch = -1;  // scan_epoch the A tails / slot records were written for
+
+  // A-side tails of the operand image and the slot records for the current components
+  void tc_tails() {
+    if (tc_tails_epoch == scan_epoch && tc_slots.p) return;
+    tc_prepare();
+    tc_slots.ensure((size_t)Tp * 16);
+    CUDA_TRY(launch_tc_tails(tc_img.p, comp.p, Tp, d, tc_slots.p, st));
+    note_launch();
+    tc_tails_epoch = scan_epoch;
+  }
+  bool capp_ready = false;
   bool tc_cap_on = false;       // caps in use for this round's scans
   bool tc_bound_only = false;   // the next tc_scan is the bound pass (writes ucap, no keys)
   bool tpmin_on = false;   // allocated and reset for this run
@@ -2218,6 +2240,7 @@ struct nnm_dataset {
     const int64_t n_up = w_end - w_begin;
     if (n_up <= 0) return;
     tc_prepare();
+    tc_tails();
     // the bound pass and the exact pass of phase 1 scan the same list: mirror + sort once
     const bool reuse = !umax && tc_list_epoch == scan_epoch && tc_list_items == items &&
                        tc_list_wb == w_begin && tc_list_we == w_end;
@@ -2278,8 +2301,10 @@ struct nnm_dataset {
     a.dump = nullptr;
     a.tpmin = tpmin_use ? tpmin.p : nullptr;
     a.ucap = tc_bound_only ? ucap.p : (tc_cap_on ? const_cast<unsigned*>(caps_read) : nullptr);
+    a.capp = (!tc_bound_only && tc_cap_on && capp_ready) ? capp.p : nullptr;
     a.bound_only = tc_bound_only ? 1 : 0;
     a.trange = tile_range.p;  // computed by this round's step 1
+    a.slots = tc_slots.p;     // slot records + A tails of this round (tc_tails)
     const char* dbg = getenv("NNM_TC_DBG");
     a.dbg = dbg ? atoi(dbg) : 0;
     const int grid = (int)std::min<int64_t>(nfull, (int64_t)sms);
@@ -2885,6 +2910,13 @@ struct nnm_dataset {
     if (rd_stage != 1) throw NnmError{NNM_E_INVALID, "staged round: phase 1 before the bound step"};
     fill_none(b1, vn);
     fill_none(b2, vn);
+    capp_ready = false;
+    if (tc_cap_on && caps_read) {  // per-position caps (staged per item by the scan)
+      capp.ensure(vn);
+      pos_caps_kernel<<<blocks_for(vn), 256, 0, st>>>(vn, comp.p, caps_read, capp.p); note_launch();
+      CUDA_TRY(cudaGetLastError());
+      capp_ready = true;
+    }
     const auto sh = share(rd_n1, rank, world);
     NvtxRange r1("nnm phase-1 scan");
     if (sh.second > sh.first)
@@ -4205,6 +4237,8 @@ int nnm_tc_probe(nnm_dataset* ds, const int32_t* items, int64_t n_items, double*
     if (!tc_supported(ds->d)) throw NnmError{NNM_E_UNSUPPORTED, "d outside the tensor-core scan"};
     ds->bv_begin(EUCLIDEAN, NAN);  // kd view, tile geometry, singleton components
     ds->tc_prepare();
+    ++ds->scan_epoch;
+    ds->tc_tails();
     for (int64_t t = 0; t < 2 * n_items; ++t)
       if (items[t] < 0 || items[t] >= ds->Tp) invalid("tile index out of range");
     DevBuf<int2> it;
@@ -4233,6 +4267,7 @@ int nnm_tc_probe(nnm_dataset* ds, const int32_t* items, int64_t n_items, double*
     a.B1 = ds->B1.p;
     a.B2 = ds->B2.p;
     a.dump = dump.p;
+    a.slots = ds->tc_slots.p;
     a.dbg = 0;
     a.trace = nullptr;
     CUDA_TRY(launch_tc_scan(a, (int)std::min<int64_t>(n_items, ds->sms), ds->st));

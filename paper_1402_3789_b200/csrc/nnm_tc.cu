@@ -46,13 +46,13 @@ namespace nnm {
 namespace {
 
 constexpr int TC_STAGES = 8;
-constexpr int TC_EPI_WARPS = 8;                        // warps 0-7: 2 groups x 4 lane quadrants
-constexpr int TC_EPI_GROUPS = 2;                       // epilogue groups, alternating items
-constexpr int TC_PREP_GROUPS = 4;                      // 4 single-warp prep groups, items q % 4
+constexpr int TC_EPI_WARPS = 12;                       // warps 0-11: 3 groups x 4 lane quadrants
+constexpr int TC_EPI_GROUPS = 3;                       // epilogue groups, items q % 3
+constexpr int TC_PREP_GROUPS = 2;                      // 2 single-warp prep groups, items q % 2
 constexpr int TC_PREP_THREADS = 32;                    // per group; each lane owns 4 rows / columns
 constexpr int TC_PRODUCER_WARP = TC_EPI_WARPS + TC_PREP_GROUPS * TC_PREP_THREADS / 32;
 constexpr int TC_MMA_WARP = TC_PRODUCER_WARP + 1;
-constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;     // 448: <= 4 warps per SMSP -> 128 regs
+constexpr int TC_THREADS = (TC_MMA_WARP + 1) * 32;     // 512: 16 warps x 128 registers
 constexpr int TC_RING = 64;                            // item ring (>> stages: see prep)
 constexpr int TC_ACC = 4;                              // TMEM accumulators (4 x 128 columns)
 constexpr uint32_t TC_TILE_BYTES = TC_TILE_FLOATS * 4;
@@ -71,15 +71,25 @@ struct TcSmem {
   int acomp[2][TILE];                  // component labels of the row / column tiles
   int bcomp[TC_STAGES][TILE];
   float asq[2][TILE];                  // |x_t|^2 of the row tile's positions
+  float atn[2][TILE];                  // |x_t| and eta of the row tile's positions
+  float aeta[2][TILE];
   float bsq[TC_STAGES][TILE];          // |y_t|^2 of the column tile's positions
+  // per-row data of the item's ROW tile, staged with every item (so the epilogue never
+  // waits on global memory at a row-tile change): component labels, the rows' global
+  // second-best keys at copy time (a valid threshold: keys only decrease) and, on capped
+  // exact passes, the per-position component caps
+  int rcomp[TC_STAGES][TILE];
+  unsigned long long rb2[TC_STAGES][TILE];
+  unsigned rcap[TC_STAGES][TILE];
   float rrow[TC_STAGES][TILE];         // per row of the item: r_i, E and eta (prep -> epilogue)
   float erow[TC_STAGES][TILE];
   float etarow[TC_STAGES][TILE];
   int2 ring[TC_RING];                  // (I, J) of item q at q % TC_RING (written by the producer)
+  int4 ringtr[TC_RING];                // component-label ranges of I and J (x, y: I; z, w: J)
   int ringrt[TC_RING];                 // row-tile index of item q, negated-minus-one when item q
                                        // is the first of its row tile (producer)
-  int slot[2][8];
-  int nslot[2];                        // distinct components of the row tile (select_slots)
+  int arec[2][16];                     // row tile's slot record: [0..7] component slots,
+                                       // [8] distinct components (tc_tails_kernel, per round)
   int chk[TC_STAGES];                  // item may hold unmasked same-component pairs (prep)
   unsigned lbw[TC_EPI_GROUPS][2][4];   // tile-pair bound: per-quadrant minima of an item
   int lbcnt[TC_EPI_GROUPS][2];         // (epilogue group, item parity) arrivals
@@ -397,30 +407,52 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
     if (lane == 0) {
       int rt = -1, prevI = -1;
       int2 nxt = __ldg(p.items + w0);
+      // component-label ranges of the item's tiles (the prep's slot-check decision), one
+      // item ahead like the item itself; no trange: always check
+      auto ranges = [&](int2 t) {
+        if (!p.trange) return make_int4(0, 0x7FFFFFFF, 0, 0x7FFFFFFF);
+        const int2 a = __ldg(p.trange + t.x), b = __ldg(p.trange + t.y);
+        return make_int4(a.x, a.y, b.x, b.y);
+      };
+      int4 nxtr = ranges(nxt);
       for (int q = 0; q < nq; ++q) {
         const int2 it = nxt;
-        if (q + 1 < nq) nxt = __ldg(p.items + w0 + q + 1);  // one item of lookahead
+        const int4 itr = nxtr;
+        if (q + 1 < nq) {  // one item of lookahead
+          nxt = __ldg(p.items + w0 + q + 1);
+          nxtr = ranges(nxt);
+        }
         if (it.x != prevI) {
           ++rt;
           prevI = it.x;
           const int xb = rt & 1;
           if (rt >= 2) mbar_wait(&S.aempty[xb], ((rt - 2) >> 1) & 1);
-          mbar_expect_tx(&S.afull[xb], TC_TILE_BYTES + TC_META * 4 + 2 * TILE * 4);
+          mbar_expect_tx(&S.afull[xb], TC_TILE_BYTES + TC_META * 4 + 4 * TILE * 4 + 64);
+          bulk_g2s(S.arec[xb], p.slots + (int64_t)it.x * 16, 64, &S.afull[xb]);
           bulk_g2s(S.A[xb], p.img + (int64_t)it.x * TC_TILE_FLOATS, TC_TILE_BYTES, &S.afull[xb]);
           bulk_g2s(S.metaA[xb], p.meta + (int64_t)it.x * TC_META, TC_META * 4, &S.afull[xb]);
           bulk_g2s(S.acomp[xb], p.comp + (int64_t)it.x * TILE, TILE * 4, &S.afull[xb]);
           bulk_g2s(S.asq[xb], p.sq + (int64_t)it.x * TILE, TILE * 4, &S.afull[xb]);
+          bulk_g2s(S.atn[xb], p.tnorm + (int64_t)it.x * TILE, TILE * 4, &S.afull[xb]);
+          bulk_g2s(S.aeta[xb], p.eta + (int64_t)it.x * TILE, TILE * 4, &S.afull[xb]);
         }
         const int s = q % TC_STAGES;
         if (q >= TC_STAGES) mbar_wait(&S.empty[s], ((q / TC_STAGES) - 1) & 1);
         trace(p, 0, q, 0);
         S.ring[q % TC_RING] = it;  // published to the other roles by the full barrier
+        S.ringtr[q % TC_RING] = itr;
         S.ringrt[q % TC_RING] = (q == 0 || it.x != S.ring[(q - 1) % TC_RING].x) ? -rt - 1 : rt;
-        mbar_expect_tx(&S.full[s], TC_TILE_BYTES + TC_META * 4 + 2 * TILE * 4);
+        const bool rows_b2 = !p.bound_only && !p.dump;
+        const bool rows_cap = rows_b2 && p.capp;
+        mbar_expect_tx(&S.full[s], TC_TILE_BYTES + TC_META * 4 + 3 * TILE * 4 +
+                                       (rows_b2 ? TILE * 8 : 0) + (rows_cap ? TILE * 4 : 0));
         bulk_g2s(S.B[s], p.img + (int64_t)it.y * TC_TILE_FLOATS, TC_TILE_BYTES, &S.full[s]);
         bulk_g2s(S.metaB[s], p.meta + (int64_t)it.y * TC_META, TC_META * 4, &S.full[s]);
         bulk_g2s(S.bcomp[s], p.comp + (int64_t)it.y * TILE, TILE * 4, &S.full[s]);
         bulk_g2s(S.bsq[s], p.sq + (int64_t)it.y * TILE, TILE * 4, &S.full[s]);
+        bulk_g2s(S.rcomp[s], p.comp + (int64_t)it.x * TILE, TILE * 4, &S.full[s]);
+        if (rows_b2) bulk_g2s(S.rb2[s], p.B2 + (int64_t)it.x * TILE, TILE * 8, &S.full[s]);
+        if (rows_cap) bulk_g2s(S.rcap[s], p.capp + (int64_t)it.x * TILE, TILE * 4, &S.full[s]);
       }
     }
   } else if (warp == TC_MMA_WARP) {
@@ -435,7 +467,7 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
           if (rt >= 0) mma_commit(&S.aempty[rt & 1]);  // previous A buffer free once its MMAs land
           ++rt;
           prevI = it.x;
-          mbar_wait(&S.aprepped[rt & 1], (rt >> 1) & 1);
+          mbar_wait(&S.afull[rt & 1], (rt >> 1) & 1);  // A tails written per round
         }
         const int a = q % TC_ACC;
         if (q >= TC_ACC) mbar_wait(&S.tempty[a], ((q / TC_ACC) - 1) & 1);
@@ -475,30 +507,14 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
       const int xb = rt & 1;
       if (I != myI) {
         myI = I;
+        // the A operand (coordinates + per-round tails) and its slot record arrive as copied
+        mbar_wait(&S.afull[xb], (rt >> 1) & 1);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          tn4[k] = __ldg(p.tnorm + (int64_t)I * TILE + pt + 32 * k);
-          eta4[k] = __ldg(p.eta + (int64_t)I * TILE + pt + 32 * k);
-        }
-        if (opens) {
-          // first item of the row tile: this group prepares the A operand
-          mbar_wait(&S.afull[xb], (rt >> 1) & 1);
-          select_slots(S.acomp[xb], S.slot[xb], &S.nslot[xb], pt, kc);
+        for (int k = 0; k < 8; ++k) slot[k] = S.arec[xb][k];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) slot[k] = S.slot[xb][k];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int row = pt + 32 * k;
-            write_tail(S.A[xb], row, d, kc, 1.f, 1.f, slot_hits(S.acomp[xb][row], slot), TC_MASK);
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (pt == 0) mbar_arrive(&S.aprepped[xb]);
-        } else {
-          // another group prepared it: wait, then take the slots
-          mbar_wait(&S.aprepped[xb], (rt >> 1) & 1);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) slot[k] = S.slot[xb][k];
+        for (int k = 0; k < 4; ++k) {  // staged with the row tile (no global latency)
+          tn4[k] = S.atn[xb][pt + 32 * k];
+          eta4[k] = S.aeta[xb][pt + 32 * k];
         }
       }
       if (p.dbg & 2) {  // timing experiment: no prep work
@@ -545,12 +561,8 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         trace(p, 5, q, 1);
         // unmasked same-component pairs are possible only if the row tile has more
         // components than slots and the two tiles' component ranges overlap
-        const int Jt = S.ring[q % TC_RING].y;
-        bool chk = S.nslot[xb] > kc;
-        if (chk && p.trange) {
-          const int2 a = __ldg(p.trange + I), b = __ldg(p.trange + Jt);
-          chk = !(b.y < a.x || a.y < b.x);
-        }
+        const int4 tr = S.ringtr[q % TC_RING];
+        const bool chk = S.arec[xb][8] > kc && !(tr.w < tr.x || tr.y < tr.z);
         S.chk[s] = chk ? 1 : 0;
       }
       if (!(p.dbg & 4)) fence_proxy_async();  // (dbg 4: timing experiment only)
@@ -576,12 +588,31 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
     float rowU = INFINITY;                // best screened upper bound of the row (bound mode)
     int ci = -1;
     int64_t g = 0;
+    // Row-tile flush of the top-2 into the global keys, split in two so that the latency of
+    // the returning atomicMin on B1 overlaps the next item's work: step 1 at the row-tile
+    // change issues it; step 2 (the displaced key into B2, a non-returning atomicMin) runs
+    // after the next item.  Both epilogue groups merge into the same rows this way.
+    bool pend = false;
+    unsigned long long pold = 0, pk1 = NONE_KEY, pk2 = NONE_KEY;
+    int64_t pg = 0;
+    auto finish_flush = [&]() {
+      if (!pend) return;
+      pend = false;
+      const unsigned long long disp = (pk1 < pold) ? pold : pk1;
+      const unsigned long long m = disp < pk2 ? disp : pk2;
+      if (key_valid(m)) atomicMin(p.B2 + pg, m);
+    };
     auto flush_row = [&]() {
       if (ci < 0 || p.dump) return;
       if (p.bound_only) {
         if (p.ucap && rowU < INFINITY) atomicMin(p.ucap + ci, __float_as_uint(rowU));
-      } else {
-        insert_top2_g(p.B1 + g, p.B2 + g, k1, k2);
+      } else if (key_valid(k1)) {
+        finish_flush();
+        pend = true;
+        pg = g;
+        pk1 = k1;
+        pk2 = k2;
+        pold = atomicMin(p.B1 + g, k1);
       }
     };
     for (int q = e; q < nq; q += TC_EPI_GROUPS) {
@@ -595,14 +626,14 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         if (prevI >= 0) flush_row();
         prevI = I;
         g = (int64_t)I * TILE + i;
-        ci = __ldg(p.comp + g);
-        if (p.bound_only) {
+        ci = S.rcomp[s][i];
+        if (p.bound_only || p.dump) {
           gT = INFINITY;
         } else {
-          const unsigned long long gb = *((volatile const unsigned long long*)(p.B2 + g));
+          const unsigned long long gb = S.rb2[s][i];
           gT = key_valid(gb) ? key_value(gb) : INFINITY;
         }
-        capT = (!p.bound_only && p.ucap && ci >= 0) ? __uint_as_float(p.ucap[ci]) : INFINITY;
+        capT = (!p.bound_only && !p.dump && p.capp && ci >= 0) ? __uint_as_float(S.rcap[s][i]) : INFINITY;
         k1 = k2 = NONE_KEY;
         tup = INFINITY;
         rowU = INFINITY;
@@ -790,8 +821,10 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
         mbar_arrive(&S.tempty[a]);
         mbar_arrive(&S.empty[s]);
       }
+      finish_flush();  // step 2 of the previous row tile's flush (its atomic has landed)
     }
     if (prevI >= 0) flush_row();
+    finish_flush();
   }
 
   tc_before();
@@ -799,6 +832,32 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
   tc_after();
   if (warp == TC_MMA_WARP)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// ---------------------------------------------------------------- per-round A tails
+// Once per round (components changed): for every tile, its component slots (the first kc
+// distinct components in position order, -2 unused) and distinct count into the slot
+// record [T][16], and the A-side K tail of every row written into the operand image:
+// (1, 1, -2^50 at each slot holding the row's component).  The scan then takes the row
+// tile as copied (no per-row-tile prep); B tails are rewritten per item in shared memory.
+__global__ void tc_tails_kernel(float* __restrict__ img, const int* __restrict__ comp, int T,
+                                int d, int* __restrict__ slots) {
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int kc = min(8, TC_K - d - 2);
+  int* rec = slots + (int64_t)t * 16;
+  const int* c = comp + (int64_t)t * TILE;
+  select_slots(c, rec, rec + 8, lane, kc);
+  int slot[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) slot[k] = rec[k];
+  float* tile = img + (int64_t)t * TC_TILE_FLOATS;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int row = lane + 32 * k;
+    write_tail(tile, row, d, kc, 1.f, 1.f, slot_hits(c[row], slot), TC_MASK);
+  }
 }
 
 // ---------------------------------------------------------------- operand image
@@ -948,6 +1007,11 @@ static cudaError_t launch_tc_d(const TcArgs& a, int grid, cudaStream_t st) {
               fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, sm, fa.localSizeBytes);
   }
   return e;
+}
+
+cudaError_t launch_tc_tails(float* img, const int* comp, int T, int d, int* slots, cudaStream_t st) {
+  tc_tails_kernel<<<(T + 7) / 8, 256, 0, st>>>(img, comp, T, d, slots);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tc_scan(const TcArgs& a, int grid, cudaStream_t st) {

@@ -39,12 +39,16 @@ struct TcArgs {
   // otherwise every row threshold is capped by its component's value (nullptr: off)
   unsigned* ucap;
   int bound_only;
+  const unsigned* capp;   // [np] per position: its component's cap (capped exact passes)
+  const int* slots;       // [T][16] per-round slot records (launch_tc_tails)
   const int2* trange;     // [T] min / max component label per tile (nullptr: always check)
 };
 
 size_t tc_smem_bytes();
 bool tc_supported(int d);
 cudaError_t launch_tc_scan(const TcArgs& a, int grid, cudaStream_t st);
+// per-round slot records + A-side operand tails for the current component labels
+cudaError_t launch_tc_tails(float* img, const int* comp, int T, int d, int* slots, cudaStream_t st);
 
 // Operand image + per-position / per-tile bounds for the kd view (once per dataset).
 cudaError_t launch_tc_prepare(const double* X64p, const int* porig, const double* tcenter64,
