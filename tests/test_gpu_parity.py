@@ -96,10 +96,13 @@ def test_run_vs_reference_engine_golden(nnm, exact_rounds):
             assert np.array_equal(rc, g[f"counters_{i}"]), i
 
 
-def test_c1_full_run_vs_reference(nnm):
-    """BASELINE config 1: 10k x 8, 5 blobs, unconstrained, P=256 (reference run here)."""
+@pytest.mark.parametrize("small", ["0", "1"])
+def test_c1_full_run_vs_reference(nnm, small, monkeypatch):
+    """BASELINE config 1: 10k x 8, 5 blobs, unconstrained, P=256 (reference run here), on
+    the general pruned path and on the dense small-input path (the default for C1)."""
     from paper_1402_3789_b200.datagen import config_dataset
 
+    monkeypatch.setenv("NNM_SMALL", small)
     g = golden("c1_run.npz")
     res = nnm.run(nnm.Dataset(values=config_dataset("c1")), nnm.RunConfig(pairs_per_batch=256))
     got = _records(res.merges)
@@ -140,9 +143,11 @@ def test_c2_analogue_rounds_vs_reference(nnm):
     assert np.array_equal(res.assignments, g["assign"])
 
 
+@pytest.mark.parametrize("small", ["0", "1"])  # general pruned path / dense small-input path
 @pytest.mark.parametrize("metric", ["euclidean", "squared-euclidean", "manhattan", "chebyshev"])
 @pytest.mark.parametrize("kind", ["blobs", "ties", "dups"])
-def test_boruvka_vs_oracle_flat(nnm, metric, kind):
+def test_boruvka_vs_oracle_flat(nnm, metric, kind, small, monkeypatch):
+    monkeypatch.setenv("NNM_SMALL", small)
     from oracle import nnm_oracle as orc
 
     rng = np.random.default_rng(hash((metric, kind)) % 2**32)
@@ -235,8 +240,10 @@ def test_multi_replica_run_equals_single(nnm, replicas, kw, monkeypatch):
     assert multi.device_stats["pairs_evaluated"] == single.device_stats["pairs_evaluated"]
 
 
+@pytest.mark.parametrize("small", ["0", "1"])
 @pytest.mark.parametrize("n", [1, 2, 3, 127, 129, 300, 2049])
-def test_boruvka_small_and_ragged_sizes(nnm, n):
+def test_boruvka_small_and_ragged_sizes(nnm, n, small, monkeypatch):
+    monkeypatch.setenv("NNM_SMALL", small)
     from oracle import nnm_oracle as orc
 
     rng = np.random.default_rng(n)
@@ -251,8 +258,11 @@ def test_boruvka_small_and_ragged_sizes(nnm, n):
         assert np.array_equal(res.assignments, a_or)
 
 
-def test_boruvka_shuffled_blobs_vs_oracle(nnm):
-    """Row-shuffled blob data (SURVEY 8d asks for a shuffled variant): kd order + pruning."""
+@pytest.mark.parametrize("small", ["0", "1"])
+def test_boruvka_shuffled_blobs_vs_oracle(nnm, small, monkeypatch):
+    """Row-shuffled blob data (SURVEY 8d asks for a shuffled variant): kd order + pruning
+    (general path) and the dense small-input path."""
+    monkeypatch.setenv("NNM_SMALL", small)
     from oracle import nnm_oracle as orc
 
     X = nnm.generate_synthetic(4000, 9, 23, 1.0, seed=7)[0]
