@@ -184,3 +184,60 @@ def test_c4_gpu_replay_equals_host_replay(nnm, c4, env):
     if env.get("NNM_GPU_REPLAY") == "0":
         assert rb.device_stats["replay_gpu_merges"] == 0
     assert a == b
+
+
+@pytest.fixture(scope="module")
+def c4_full(nnm, c4):
+    return nnm.fit(c4)
+
+
+def test_c4_dmax_and_kl1_are_prefixes_of_the_full_dendrogram(nnm, c4, c4_full):
+    """Single linkage: with dmax the merge list is the prefix of merges with height <= dmax
+    (the MSF of the eligible graph, pairgen.py:197-198 / oracle.py:82-83); with kl1 it is
+    the first n - kl1 merges (engine.py:139-142).  Checked at 2M against the full run."""
+    full = c4_full.merges.array
+    dmax = float(np.sqrt(full["dist"][1_500_000] * full["dist"][1_500_001]))  # between two merges
+    part = nnm.fit(c4, dmax=dmax)
+    k = int(np.searchsorted(full["dist"], dmax, side="right"))
+    assert len(part.merges) == k
+    for f in FIELDS:
+        assert np.array_equal(part.merges.array[f], full[f][:k]), f
+    kl1 = 4000
+    trunc = nnm.fit(c4, kl1=kl1)
+    assert len(trunc.merges) == c4.shape[0] - kl1
+    for f in FIELDS:
+        assert np.array_equal(trunc.merges.array[f], full[f][: c4.shape[0] - kl1]), f
+    assert trunc.stop_reason == "kl1-reached" and len(np.unique(trunc.assignments)) == kl1
+
+
+def test_c4_row_shuffled_same_dendrogram(nnm, c4, c4_full):
+    """the row-shuffled C4 input (default_rng(seed + 100)) gives the same
+    dendrogram: identical merge heights in order and the same point pairs (mapped back);
+    blob data has no exact distance ties, so the order is fully determined."""
+    perm = np.random.default_rng(5 + 100).permutation(c4.shape[0])
+    res = nnm.fit(np.ascontiguousarray(c4[perm]))
+    got, want = res.merges.array, c4_full.merges.array
+    assert np.array_equal(got["dist"], want["dist"])
+    a, b = perm[got["point_a"]], perm[got["point_b"]]
+    pairs = np.stack([np.minimum(a, b), np.maximum(a, b)], 1)
+    assert np.array_equal(pairs, np.stack([want["point_a"], want["point_b"]], 1))
+    assert np.array_equal(got["new_size"], want["new_size"])
+
+
+@pytest.mark.parametrize("metric", ["euclidean", "manhattan", "chebyshev"])
+def test_dense_fp64_vs_pruned_screen_heavy_ties(nnm, metric, monkeypatch):
+    """Two independent GPU algorithms on 48k points of an integer grid with duplicates
+    (massive exact ties): the pruned, screened default path against the dense exact FP64
+    Boruvka (NNM_SMALL=1, no screening, no pruning) -- identical merge logs and labels."""
+    rng = np.random.default_rng(17)
+    base = rng.integers(-20, 21, size=(24_000, 6)).astype(np.float64)
+    X = np.ascontiguousarray(np.vstack([base, base[rng.permutation(len(base))]]))
+    for cons in ({}, {"dmax": 2.0}, {"dmax": 0.0}, {"kl1": 300}):
+        monkeypatch.setenv("NNM_SMALL", "0")
+        a = nnm.fit(X, metric=metric, **cons)
+        monkeypatch.setenv("NNM_SMALL", "1")
+        b = nnm.fit(X, metric=metric, **cons)
+        for f in FIELDS:
+            assert np.array_equal(a.merges.array[f], b.merges.array[f]), (cons, f)
+        assert np.array_equal(a.assignments, b.assignments), cons
+        assert a.stop_reason == b.stop_reason
