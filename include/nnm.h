@@ -110,6 +110,13 @@ int nnm_abi_version(void);
 const char *nnm_last_error(void);
 int nnm_device_count(int32_t *out);
 
+/* Page-locked host blocks (recycled process-wide).  nnm_run / nnm_bv_end detect
+ * page-locked out_merges / out_assign: the GPU then lays out the merge records and
+ * labels itself and the copy engine writes them (no host assembly pass).  Plain
+ * (pageable) output arrays keep working; this is an optimisation only. */
+int nnm_host_alloc(int64_t bytes, void **out);
+int nnm_host_free(void *p);
+
 /* Upload X (n x d, row-major float64, finite) to `device` and build the FP32
  * screening tiles.  Replaces Dataset's array being read by every scan task
  * (model.py:29-76; pairgen.py:247-298).  Validation as Dataset.__post_init__. */

@@ -38,7 +38,8 @@ EXPORTED = (
     "nnm_pairwise", "nnm_bv_begin", "nnm_bv_scan", "nnm_bv_round_bound", "nnm_bv_round_phase1",
     "nnm_bv_round_phase2", "nnm_bv_cache_scatter", "nnm_bv_second", "nnm_bv_finish_round",
     "nnm_bv_end", "nnm_measure_fp32_peak", "nnm_tc_probe", "nnm_csv_load", "nnm_csv_fetch",
-    "nnm_csv_free", "nnm_first_nonfinite", "nnm_round_log", "nnm_run_multi",
+    "nnm_csv_free", "nnm_first_nonfinite", "nnm_round_log", "nnm_run_multi", "nnm_host_alloc",
+    "nnm_host_free",
 )
 
 
@@ -145,6 +146,8 @@ def load():
         lib.nnm_bv_end.argtypes = [vp, i64, vp, P(i64), vp, P(i64), P(i32), P(Stats)]
         lib.nnm_measure_fp32_peak.argtypes = [i32, P(dbl)]
         lib.nnm_round_log.argtypes = [vp, vp, i64, P(i64)]
+        lib.nnm_host_alloc.argtypes = [i64, P(vp)]
+        lib.nnm_host_free.argtypes = [vp]
         for name in EXPORTED:
             if name not in ("nnm_abi_version", "nnm_last_error"):
                 getattr(lib, name).restype = ctypes.c_int
@@ -158,6 +161,46 @@ def first_nonfinite(values: np.ndarray) -> int:
     out = ctypes.c_int64(-1)
     check(lib.nnm_first_nonfinite(values.ctypes.data, int(values.size), 0, ctypes.byref(out)))
     return int(out.value)
+
+
+HOST_OUT_MIN = 1 << 22        # smaller outputs stay ordinary numpy arrays
+HOST_OUT_CAP = 8 << 30        # page-locked output bytes alive at once (then ordinary arrays)
+_host_out = 0
+
+
+def _host_release(addr: int, nbytes: int) -> None:
+    global _host_out
+    with _lock:
+        _host_out -= nbytes
+    if _lib is not None:
+        _lib.nnm_host_free(addr)
+
+
+def host_empty(count: int, dtype) -> np.ndarray:
+    """Uninitialised 1-D output array, page-locked when large (nnm_host_alloc).
+
+    libnnm detects page-locked merge / label outputs and has the GPU lay the records out
+    and the copy engine write them (include/nnm.h).  The block returns to libnnm's pool
+    when the last view of the array dies.  Falls back to an ordinary array when small,
+    when the cap is reached or when no device is present."""
+    global _host_out
+    dtype = np.dtype(dtype)
+    count = int(count)
+    nbytes = count * dtype.itemsize
+    if nbytes < HOST_OUT_MIN or gpu_count() == 0:
+        return np.empty(count, dtype)
+    with _lock:
+        if _host_out + nbytes > HOST_OUT_CAP:
+            return np.empty(count, dtype)
+        _host_out += nbytes
+    p = ctypes.c_void_p()
+    if load().nnm_host_alloc(nbytes, ctypes.byref(p)) != NNM_OK or not p.value:
+        with _lock:
+            _host_out -= nbytes
+        return np.empty(count, dtype)
+    buf = (ctypes.c_char * nbytes).from_address(p.value)
+    weakref.finalize(buf, _host_release, p.value, nbytes)
+    return np.frombuffer(buf, dtype=dtype, count=count)
 
 
 def check(rc: int) -> None:

@@ -154,6 +154,22 @@ PinnedPool& pinned_pool() {
   return *pool;
 }
 
+// blocks handed to callers through nnm_host_alloc (size needed to recycle them)
+std::mutex g_host_mu;
+std::map<void*, size_t> g_host_blocks;
+
+// page-locked (cudaMallocHost / cudaHostRegister) host memory: the copy engine can write
+// the run's outputs there directly
+bool is_page_locked(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 template <class T>
 struct PinnedBuf {  // grow-only page-locked host staging buffer (blocks from pinned_pool)
   T* p = nullptr;
@@ -452,6 +468,46 @@ __global__ void replay_edges_kernel(const Edge* __restrict__ e, int64_t ne, int 
   out[t] = r;
 }
 
+// merge records [0, m) of the GPU replay, laid out as the caller's nnm_merge array
+// (copied into page-locked output by the copy engine; nnm_api bv_end)
+__global__ void merge_records_kernel(const ReplayEdge* __restrict__ e, int64_t m,
+                                     const int* __restrict__ rk, const int* __restrict__ rd,
+                                     const int* __restrict__ rs, nnm_merge* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const ReplayEdge x = e[k];
+  nnm_merge r;
+  r.round = x.round;
+  r.root_a = rk[k];
+  r.root_b = rd[k];
+  r.dist = x.dist;
+  r.new_size = rs[k];
+  r.point_a = x.a;
+  r.point_b = x.b;
+  out[k] = r;
+}
+
+// the host tail's links (dropped root -> kept root, kept < dropped) onto the GPU forest
+__global__ void apply_links_kernel(const int2* __restrict__ links, int64_t cnt, int* par) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < cnt) par[links[t].x] = links[t].y;
+}
+
+// final labels (root = minimum index of the cluster, model.py:148-160) as int64; links
+// only point to smaller indices, so concurrent path halving is benign
+__global__ void assign64_kernel(int64_t n, int* par, int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int x = (int)i, p = par[x];
+  while (p != x) {
+    const int g = par[p];
+    if (g != p) par[x] = g;
+    x = g;
+    p = par[x];
+  }
+  out[i] = x;
+}
+
 __global__ void hook_kernel(int n, const int* __restrict__ comp,
                             const unsigned long long* __restrict__ cmin_d,
                             const unsigned long long* __restrict__ cmin_ab, int* parent,
@@ -677,6 +733,294 @@ __global__ void __launch_bounds__(256) small_boruvka_kernel(
     const unsigned long long added = *((volatile unsigned long long*)(ctl + 1));
     grid.sync();
     if (tid == 0) ctl[1] = 0;
+    if (added == 0) break;
+    grid.sync();
+  }
+  if (tid == 0) ctl[3] = (unsigned long long)round;
+}
+
+// ---- screened Boruvka for small inputs: ONE cooperative launch for all rounds -----------
+// The same round as small_boruvka_kernel, with the row minima found by an FP32 screen and
+// certified in FP64 (the error model of nnm_common.cuh):
+//   sweep    work units of (R rows) x (SMALL_CW columns) spread over every warp of the
+//            grid; per unit and row the smallest and second smallest screened value
+//            v1 <= v2 over the cross-component columns (FP32 direct differences, X32 SoA,
+//            column data straight from L1/L2) and the column j1 of v1 -> partials;
+//   certify  per row the top-2 over its partials, S1 = exact(i, j1) (scipy order),
+//            U = S1 if S1 <= thr else thr.  Every column j with S_j <= U has
+//            v_j <= screen_upper(U, R_i) =: B, so v2 > B proves j1 the unique minimum (or,
+//            when S1 > thr, that no column is eligible);
+//   resolve  rows with v2 <= B (ties, duplicates) -- one warp per row over every column
+//            with v_j <= B, exact keys, lexicographic (d, a, b) minimum (model.py:100-106).
+// R_i = norm(x_i) + max norm bounds norm(x_i) + norm(x_j) for every j.  Component minima,
+// hooking, root finding and relabelling follow as in small_boruvka_kernel, with the
+// pointer jumping replaced by a read-only walk to the root (one grid barrier).
+constexpr int SMALL_CW = 1024;       // columns per work unit
+constexpr int SMALL_AUTO_N = 16384;  // default-on size limit (n^2 work per round)
+template <int M, int D, int R>
+__global__ void __launch_bounds__(256) small_screened_kernel(
+    const double* __restrict__ X, const float* __restrict__ X32, int64_t ld, int n, int d,
+    double thr, const double* __restrict__ norm, double maxnorm, ErrModel em, int max_rounds,
+    int* comp, int* parent, unsigned long long* rbd, unsigned long long* rbab,
+    unsigned long long* cmd, unsigned long long* cmab, Edge* edges, unsigned long long* ctl,
+    float* pv1, float* pv2, int* pj1, int* needl, int* rootof, float2* ndup) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nth >> 5;
+  const int C = (n + SMALL_CW - 1) / SMALL_CW, G = (n + R - 1) / R;
+  for (int i = tid; i < n; i += nth) {
+    comp[i] = i;
+    cmd[i] = cmab[i] = NONE_KEY;
+  }
+  if (tid == 0) ctl[5] = 0;
+  // packed negated columns {-x, -x}, SoA [D][n]: a warp's 64-bit loads of one coordinate
+  // are 256 contiguous bytes; each feeds the FADD2 of two rows
+  if (M == EUCLIDEAN || M == SQEUCLIDEAN)
+    for (int64_t q = tid; q < (int64_t)D * n; q += nth) {
+      const int k = (int)(q / n), j = (int)(q - (int64_t)k * n);
+      const float x = k < d ? -X32[(int64_t)k * ld + j] : 0.f;
+      ndup[q] = make_float2(x, x);
+    }
+  grid.sync();
+  auto screened = [&](const float* xi, int j) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float tt = xi[k] - (k < d ? __ldg(X32 + (int64_t)k * ld + j) : 0.f);
+      if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc = __fmaf_rn(tt, tt, acc);
+      else if (M == MANHATTAN) acc += fabsf(tt);
+      else acc = fmaxf(acc, fabsf(tt));
+    }
+    return acc;
+  };
+  auto exact = [&](int i, int j) {
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) {  // scipy order (metrics.py:67-73)
+      const double tt = __dsub_rn(X[(int64_t)i * d + k], X[(int64_t)j * d + k]);
+      if (M == EUCLIDEAN || M == SQEUCLIDEAN) acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+      else if (M == MANHATTAN) acc = __dadd_rn(acc, fabs(tt));
+      else acc = fmax(acc, fabs(tt));
+    }
+    return acc;
+  };
+  auto pack = [](int i, int j) {
+    return ((unsigned long long)min(i, j) << 32) | (unsigned)max(i, j);
+  };
+  int round = 0;
+  while (round < max_rounds) {
+    // sweep: screened top-2 per (row, column chunk)
+    unsigned long long evals = 0;
+    for (int u = gw; u < G * C; u += nw) {
+      const int g = u / C, c = u - g * C;
+      const int i0 = g * R, jb = c * SMALL_CW, je = min(n, jb + SMALL_CW);
+      float2 xi2[R / 2][D];  // rows (2p, 2p + 1) packed
+      int ci[R];
+      float v1[R], v2[R];
+      int j1[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = i0 + r;
+        ci[r] = i < n ? comp[i] : -3;
+        v1[r] = v2[r] = INFINITY;
+        j1[r] = -1;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const float x = (i < n && k < d) ? X32[(int64_t)k * ld + i] : 0.f;
+          if (r & 1) xi2[r >> 1][k].y = x;
+          else xi2[r >> 1][k].x = x;
+        }
+      }
+      for (int j = jb + lane; j < je; j += 32) {
+        const int cj = __ldg(comp + j);
+        float v[R];
+        if (M == EUCLIDEAN || M == SQEUCLIDEAN) {
+          float2 nx[D];
+          const float2* col = ndup + j;
+#pragma unroll
+          for (int k = 0; k < D; ++k) nx[k] = __ldg(col + (int64_t)k * n);
+#pragma unroll
+          for (int p = 0; p < R / 2; ++p) {  // two rows per packed FADD2 / FFMA2
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              const float2 tt = __fadd2_rn(xi2[p][k], nx[k]);
+              acc = __ffma2_rn(tt, tt, acc);
+            }
+            v[2 * p] = acc.x;
+            v[2 * p + 1] = acc.y;
+          }
+        } else {
+          float xj[D];
+#pragma unroll
+          for (int k = 0; k < D; ++k) xj[k] = k < d ? __ldg(X32 + (int64_t)k * ld + j) : 0.f;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              const float tt = (r & 1 ? xi2[r >> 1][k].y : xi2[r >> 1][k].x) - xj[k];
+              if (M == MANHATTAN) acc += fabsf(tt);
+              else acc = fmaxf(acc, fabsf(tt));
+            }
+            v[r] = acc;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {  // branch-free top-2 over the cross columns
+          const bool cross = cj != ci[r] && ci[r] != -3;
+          evals += cross;
+          const float x = cross ? v[r] : INFINITY;
+          const bool lt = x < v1[r];
+          v2[r] = lt ? v1[r] : fminf(v2[r], x);
+          j1[r] = lt ? j : j1[r];
+          v1[r] = fminf(v1[r], x);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float a1 = v1[r], a2 = v2[r];
+        int aj = j1[r];
+        for (int o = 16; o > 0; o >>= 1) {
+          const float b1 = __shfl_xor_sync(0xFFFFFFFFu, a1, o);
+          const float b2 = __shfl_xor_sync(0xFFFFFFFFu, a2, o);
+          const int bj = __shfl_xor_sync(0xFFFFFFFFu, aj, o);
+          const bool take = b1 < a1 || (b1 == a1 && bj >= 0 && (aj < 0 || bj < aj));
+          a2 = fminf(fmaxf(a1, b1), fminf(a2, b2));
+          a1 = fminf(a1, b1);
+          aj = take ? bj : aj;
+        }
+        const int i = i0 + r;
+        if (lane == 0 && i < n) {
+          pv1[(int64_t)c * n + i] = a1;
+          pv2[(int64_t)c * n + i] = a2;
+          pj1[(int64_t)c * n + i] = aj;
+        }
+      }
+    }
+    evals = __reduce_add_sync(0xFFFFFFFFu, (unsigned)evals);
+    if (lane == 0 && evals) atomicAdd(ctl + 4, evals);
+    grid.sync();
+    // certify: one thread per row
+    for (int i = tid; i < n; i += nth) {
+      float a1 = INFINITY, a2 = INFINITY;
+      int aj = -1;
+      for (int c = 0; c < C; ++c) {
+        const float b1 = pv1[(int64_t)c * n + i], b2 = pv2[(int64_t)c * n + i];
+        const int bj = pj1[(int64_t)c * n + i];
+        const bool take = b1 < a1 || (b1 == a1 && bj >= 0 && (aj < 0 || bj < aj));
+        a2 = fminf(fmaxf(a1, b1), fminf(a2, b2));
+        a1 = fminf(a1, b1);
+        aj = take ? bj : aj;
+      }
+      unsigned long long kd = NONE_KEY, kab = NONE_KEY;
+      if (aj >= 0) {
+        const double S1 = exact(i, aj);
+        const double U = S1 <= thr ? S1 : thr;
+        const double B = screen_upper(em, U, norm[i] + maxnorm);
+        if ((double)a2 > B) {
+          if (S1 <= thr) {
+            kd = dbits(S1);
+            kab = pack(i, aj);
+          }
+        } else {
+          needl[atomicAdd((int*)(ctl + 5), 1)] = i;
+          rbd[i] = dbits(B);  // the bound, for the resolve step
+          continue;
+        }
+      }
+      rbd[i] = kd;
+      rbab[i] = kab;
+      if (kd != NONE_KEY) atomicMin(cmd + comp[i], kd);
+    }
+    grid.sync();
+    // resolve (ties / near ties): one warp per listed row over every column
+    const int nneed = *((volatile int*)(ctl + 5));
+    if (nneed > 0) {
+      for (int q = gw; q < nneed; q += nw) {
+        const int i = needl[q], ci = comp[i];
+        const double B = bitsd(rbd[i]);
+        float xi[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) xi[k] = k < d ? X32[(int64_t)k * ld + i] : 0.f;
+        unsigned long long b1 = NONE_KEY, b2 = NONE_KEY;
+        for (int j = lane; j < n; j += 32) {
+          if (__ldg(comp + j) == ci) continue;
+          if ((double)screened(xi, j) > B) continue;
+          const double S = exact(i, j);
+          if (!(S <= thr)) continue;
+          const unsigned long long k1 = dbits(S), k2 = pack(i, j);
+          if (k1 < b1 || (k1 == b1 && k2 < b2)) {
+            b1 = k1;
+            b2 = k2;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long od = __shfl_xor_sync(0xFFFFFFFFu, b1, o);
+          const unsigned long long oab = __shfl_xor_sync(0xFFFFFFFFu, b2, o);
+          if (od < b1 || (od == b1 && oab < b2)) {
+            b1 = od;
+            b2 = oab;
+          }
+        }
+        if (lane == 0) {
+          rbd[i] = b1;
+          rbab[i] = b2;
+          if (b1 != NONE_KEY) atomicMin(cmd + ci, b1);
+        }
+      }
+      grid.sync();
+    }
+    // component minimum (d, a, b)
+    for (int i = tid; i < n; i += nth) {
+      const int ci = comp[i];
+      if (rbd[i] != NONE_KEY && rbd[i] == cmd[ci]) atomicMin(cmab + ci, rbab[i]);
+    }
+    grid.sync();
+    // hook (roots: comp[c] == c); each MST edge recorded once
+    for (int c = tid; c < n; c += nth) {
+      if (comp[c] != c) continue;
+      const unsigned long long e = cmab[c];
+      if (e == NONE_KEY) {
+        parent[c] = c;
+        continue;
+      }
+      const int a = (int)(e >> 32), b = (int)(e & 0xFFFFFFFFull);
+      const int other = comp[a] == c ? comp[b] : comp[a];
+      const bool mutual = cmab[other] == e;
+      parent[c] = (mutual && c < other) ? c : other;
+      if (!mutual || c < other) {
+        const unsigned long long at = atomicAdd(ctl + 0, 1ull);
+        Edge ed;
+        ed.d = bitsd(cmd[c]);
+        ed.a = a;
+        ed.b = b;
+        ed.round = round + 1;
+        ed.pad = 0;
+        edges[at] = ed;
+        atomicAdd(ctl + 1, 1ull);
+      }
+    }
+    grid.sync();
+    // roots: a read-only walk up the hook forest (its links are final)
+    for (int c = tid; c < n; c += nth) {
+      if (comp[c] != c) continue;
+      int x = c;
+      while (parent[x] != x) x = parent[x];
+      rootof[c] = x;
+    }
+    const unsigned long long added = *((volatile unsigned long long*)(ctl + 1));
+    grid.sync();
+    // relabel, reset the component minima and the per-round counters
+    for (int i = tid; i < n; i += nth) {
+      comp[i] = rootof[comp[i]];
+      cmd[i] = cmab[i] = NONE_KEY;
+    }
+    if (tid == 0) {
+      ctl[1] = 0;
+      ctl[5] = 0;
+    }
+    ++round;
     if (added == 0) break;
     grid.sync();
   }
@@ -2119,15 +2463,17 @@ struct nnm_dataset {
   const void* rp_e = nullptr;
   ReplayState rp_state{};
   // host replay scratch (reused across runs; faulted in during the GPU rounds by nnm_run)
-  std::vector<int32_t> rp_par, rp_sz, rp_keep, rp_drop, rp_size;
+  DevBuf<float> sm_v1, sm_v2;      // small_screened_kernel partials
+  DevBuf<int> sm_j1, sm_need;
+  DevBuf<float2> sm_dup;
+  PinnedBuf<int32_t> rp_par, rp_sz;
+  PinnedBuf<int2> rp_links;        // host tail links (dropped -> kept) for the GPU labels
+  DevBuf<nnm_merge> rec_dev;       // merge records staged for page-locked output
+  DevBuf<int64_t> as_dev;          // labels staged for page-locked output
+  DevBuf<int2> links_dev;
   void replay_host_buffers() {
-    if ((int64_t)rp_par.size() < n) {
-      rp_par.resize(n);
-      rp_sz.resize(n);
-      rp_keep.resize(n);
-      rp_drop.resize(n);
-      rp_size.resize(n);
-    }
+    rp_par.ensure(std::max<int64_t>(n, 1));
+    rp_sz.ensure(std::max<int64_t>(n, 1));
   }
   DevBuf<int2> pairs;
   DevBuf<double> pair_d;
@@ -3310,7 +3656,11 @@ struct nnm_dataset {
 
   // dense exact Boruvka for small inputs (small_boruvka_kernel); leaves the MST edges in
   // `edges` / counters[0] for bv_end.  Returns false when the device cannot run it.
-  bool small_boruvka(int metric, double dmax) {
+  bool small_boruvka(int metric, double dmax, bool screened) {
+    if (screened) {
+      ensure_norms(metric);
+      if (!(maxnorm < 1e30)) return false;  // FP32 coordinates could overflow: general path
+    }
     bv_metric = metric;
     bv_round = 0;
     const double thr = std::isnan(dmax) ? INFINITY : (metric == EUCLIDEAN ? dmax * dmax : dmax);
@@ -3324,7 +3674,23 @@ struct nnm_dataset {
     counters.ensure(8);
     CUDA_TRY(cudaMemsetAsync(counters.p, 0, 8 * sizeof(unsigned long long), st));
     void* kfn = nullptr;
-    if (d <= 8) {
+    if (screened) {
+      if (d <= 8) {
+        switch (metric) {
+          case MANHATTAN: kfn = (void*)small_screened_kernel<MANHATTAN, 8, 8>; break;
+          case CHEBYSHEV: kfn = (void*)small_screened_kernel<CHEBYSHEV, 8, 8>; break;
+          default: kfn = (void*)small_screened_kernel<EUCLIDEAN, 8, 8>;
+        }
+      } else if (d <= 16) {
+        switch (metric) {
+          case MANHATTAN: kfn = (void*)small_screened_kernel<MANHATTAN, 16, 4>; break;
+          case CHEBYSHEV: kfn = (void*)small_screened_kernel<CHEBYSHEV, 16, 4>; break;
+          default: kfn = (void*)small_screened_kernel<EUCLIDEAN, 16, 4>;
+        }
+      } else {
+        return false;
+      }
+    } else if (d <= 8) {
       switch (metric) {
         case MANHATTAN: kfn = (void*)small_boruvka_kernel<MANHATTAN, 8, 4>; break;
         case CHEBYSHEV: kfn = (void*)small_boruvka_kernel<CHEBYSHEV, 8, 4>; break;
@@ -3343,7 +3709,12 @@ struct nnm_dataset {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, 256, 0));
     if (occ < 1) return false;
     const int rpb = d <= 8 ? 32 : 16;
-    const int grid = std::min(sms * occ, std::max(1, (int)((n + rpb - 1) / rpb)));
+    int64_t want = (n + rpb - 1) / rpb;  // dense: row passes of 8 warps x R rows
+    if (screened) {  // work units of R rows x SMALL_CW columns, 8 warps per block
+      const int64_t R = d <= 8 ? 8 : 4;
+      want = ((n + R - 1) / R * ((n + SMALL_CW - 1) / SMALL_CW) + 7) / 8;
+    }
+    const int grid = (int)std::min<int64_t>(sms * occ, std::max<int64_t>(1, want));
     const double* x = X64.p;
     int nn = (int)n, dd = d, maxr = 64;
     int *pc = comp.p, *pp = parent.p;
@@ -3352,8 +3723,33 @@ struct nnm_dataset {
     Edge* pe = edges.p;
     double th = thr;
     void* args[] = {&x, &nn, &dd, &th, &maxr, &pc, &pp, &prbd, &prbab, &pcmd, &pcmab, &pe, &pctl};
+    const float* x32 = X32.p;
+    int64_t ldd = ld;
+    const double* pn = norm.p;
+    double mn = maxnorm;
+    ErrModel e = make_err_model(metric, d);
+    float *ppv1 = nullptr, *ppv2 = nullptr;
+    int *ppj1 = nullptr, *pneed = nullptr, *proot = nullptr;
+    float2* pdup = nullptr;
+    if (screened) {
+      sm_dup.ensure((size_t)n * (d <= 8 ? 8 : 16));
+      pdup = sm_dup.p;
+      const int64_t parts = (n + SMALL_CW - 1) / SMALL_CW * n;
+      sm_v1.ensure(parts);
+      sm_v2.ensure(parts);
+      sm_j1.ensure(parts);
+      sm_need.ensure(n);
+      resc.ensure(n);
+      ppv1 = sm_v1.p;
+      ppv2 = sm_v2.p;
+      ppj1 = sm_j1.p;
+      pneed = sm_need.p;
+      proot = resc.p;
+    }
+    void* sargs[] = {&x, &x32, &ldd, &nn, &dd, &th, &pn, &mn, &e, &maxr, &pc, &pp,
+                     &prbd, &prbab, &pcmd, &pcmab, &pe, &pctl, &ppv1, &ppv2, &ppj1, &pneed, &proot, &pdup};
     CUDA_TRY(cudaEventRecord(ev0, st));
-    CUDA_TRY(cudaLaunchCooperativeKernel(kfn, grid, 256, args, 0, st));
+    CUDA_TRY(cudaLaunchCooperativeKernel(kfn, grid, 256, screened ? sargs : args, 0, st));
     note_launch();
     CUDA_TRY(cudaEventRecord(ev1, st));
     unsigned long long h[5];
@@ -3390,6 +3786,13 @@ struct nnm_dataset {
     const int64_t m = stop_of(n) ? 0 : std::min<int64_t>((int64_t)ne, std::max<int64_t>(n - floor_count, 0));
     auto tq0 = std::chrono::steady_clock::now();
     ReplayEdge* h = nullptr;
+    const char* ge = getenv("NNM_GPU_REPLAY");
+    const bool gpu = m >= 32768 && !(ge && ge[0] == '0');
+    // page-locked outputs (nnm_host_alloc, the engine's default): the GPU writes the merge
+    // records and labels and the copy engine moves them; the host only replays a tail
+    const char* pe_ = getenv("NNM_PINNED_OUT");
+    const bool pin_out = gpu && !(pe_ && pe_[0] == '0') && is_page_locked(out) &&
+                         is_page_locked(assign);
     if (ne > 0) {
       thrust::sort(thrust::cuda::par(talloc).on(st), edges.p, edges.p + ne, EdgeLess());
       replay.ensure(ne);
@@ -3398,10 +3801,12 @@ struct nnm_dataset {
                                                                    replay.p); note_launch();
       CUDA_TRY(cudaGetLastError());
       h = host_replay.ensure(ne);
-      // the 24-byte records travel on the side stream while the replay kernels run
-      CUDA_TRY(cudaEventRecord(ev2, st));
-      CUDA_TRY(cudaStreamWaitEvent(st2, ev2, 0));
-      CUDA_TRY(cudaMemcpyAsync(h, replay.p, ne * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st2));
+      if (!pin_out) {
+        // the 24-byte records travel on the side stream while the replay kernels run
+        CUDA_TRY(cudaEventRecord(ev2, st));
+        CUDA_TRY(cudaStreamWaitEvent(st2, ev2, 0));
+        CUDA_TRY(cudaMemcpyAsync(h, replay.p, ne * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st2));
+      }
     }
     const bool dbg = getenv("NNM_DEBUG") != nullptr;
     auto lap = [&](const char* what) {
@@ -3416,11 +3821,11 @@ struct nnm_dataset {
     int32_t* RS = h_rs.ensure(std::max<int64_t>(m, 1));
     int32_t* AS = nullptr;  // labels from the GPU (nullptr: host finds)
     int64_t host_from = 0;  // first merge replayed on the host
-    const char* ge = getenv("NNM_GPU_REPLAY");
-    const bool gpu = m >= 32768 && !(ge && ge[0] == '0');
-    std::vector<int32_t>& par = rp_par;
-    std::vector<int32_t>& sz = rp_sz;
+    int64_t rec_from = 0;   // first merge record the host writes
+    bool gpu_assign = false;  // labels written to `assign` by the copy engine
     replay_host_buffers();
+    int32_t* par = rp_par.p;
+    int32_t* sz = rp_sz.p;
     auto tq1 = tq0;
     if (gpu) {
       const char* ce = getenv("NNM_REPLAY_CHUNKS");
@@ -3519,21 +3924,51 @@ struct nnm_dataset {
       if (ctl[3]) throw NnmError{NNM_E_CUDA, "boruvka produced a cycle (internal error)"};
       host_from = ctl[1] < 0 ? m : ctl[1];
       stats.replay_gpu_merges = host_from;
-      if (host_from > 0) {
-        CUDA_TRY(cudaMemcpyAsync(RK, r_rk.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(RD, r_rd.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(RS, r_rs.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      if (pin_out) {
+        // the host tail needs the forest as the GPU left it and its own edges (side stream)
+        if (host_from < m) {
+          CUDA_TRY(cudaMemcpyAsync(par, r_par.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st2));
+          CUDA_TRY(cudaMemcpyAsync(sz, r_sz.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st2));
+          CUDA_TRY(cudaMemcpyAsync(h + host_from, replay.p + host_from,
+                                   (m - host_from) * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st2));
+        }
+        // records [0, host_from) on the GPU, straight into the caller's page-locked array
+        if (host_from > 0) {
+          rec_dev.ensure(host_from);
+          merge_records_kernel<<<blocks_for(host_from), 256, 0, st>>>(replay.p, host_from, r_rk.p,
+                                                                      r_rd.p, r_rs.p, rec_dev.p);
+          note_launch();
+          CUDA_TRY(cudaGetLastError());
+          CUDA_TRY(cudaMemcpyAsync(out, rec_dev.p, host_from * sizeof(nnm_merge),
+                                   cudaMemcpyDeviceToHost, st));
+        }
+        rec_from = host_from;
+        gpu_assign = true;
+        if (host_from == m) {
+          as_dev.ensure(n);
+          assign64_kernel<<<blocks_for(n), 256, 0, st>>>(n, r_par.p, as_dev.p);
+          note_launch();
+          CUDA_TRY(cudaGetLastError());
+          CUDA_TRY(cudaMemcpyAsync(assign, as_dev.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st2));
+      } else {
+        if (host_from > 0) {
+          CUDA_TRY(cudaMemcpyAsync(RK, r_rk.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+          CUDA_TRY(cudaMemcpyAsync(RD, r_rd.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+          CUDA_TRY(cudaMemcpyAsync(RS, r_rs.p, host_from * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        }
+        if (host_from == m) {
+          AS = h_as.ensure(n);
+          CUDA_TRY(replay_assign(n, rs, r_lab.p, st));
+          note_launch();
+          CUDA_TRY(cudaMemcpyAsync(AS, r_lab.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        } else {  // host finishes: the forest as the GPU left it (state at chunk start)
+          CUDA_TRY(cudaMemcpyAsync(par, r_par.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+          CUDA_TRY(cudaMemcpyAsync(sz, r_sz.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        }
+        sync();
       }
-      if (host_from == m) {
-        AS = h_as.ensure(n);
-        CUDA_TRY(replay_assign(n, rs, r_lab.p, st));
-        note_launch();
-        CUDA_TRY(cudaMemcpyAsync(AS, r_lab.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      } else {  // host finishes: the forest as the GPU left it (state at chunk start)
-        CUDA_TRY(cudaMemcpyAsync(par.data(), r_par.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpyAsync(sz.data(), r_sz.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      }
-      sync();
       if (dbg)
         fprintf(stderr, "[nnm] gpu replay: %lld of %lld merges, %lld chunks, longest component %d\n",
                 (long long)host_from, (long long)m, (long long)nch, ctl[2]);
@@ -3553,6 +3988,7 @@ struct nnm_dataset {
         }
         return x;
       };
+      int2* links = pin_out ? rp_links.ensure(m - host_from) : nullptr;
       constexpr int64_t kAhead = 16;  // prefetch the forest entries of later merges
       for (int64_t t = host_from; t < m; ++t) {
         if (t + kAhead < m) {
@@ -3568,16 +4004,30 @@ struct nnm_dataset {
         RK[t] = keep;
         RD[t] = drop;
         RS[t] = sz[keep];
+        if (links) links[t - host_from] = make_int2(drop, keep);
+      }
+      if (pin_out) {  // labels on the GPU: its forest plus the tail's links
+        const int64_t nl = m - host_from;
+        links_dev.ensure(nl);
+        as_dev.ensure(n);
+        CUDA_TRY(cudaMemcpyAsync(links_dev.p, links, nl * sizeof(int2), cudaMemcpyHostToDevice, st));
+        apply_links_kernel<<<blocks_for(nl), 256, 0, st>>>(links_dev.p, nl, r_par.p);
+        assign64_kernel<<<blocks_for(n), 256, 0, st>>>(n, r_par.p, as_dev.p);
+        g_launches.fetch_add(2, std::memory_order_relaxed);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaMemcpyAsync(assign, as_dev.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
       }
     }
     const int64_t nm = m;
     const int reason = (n > 0 && stop_of(n - nm)) ? stop_of(n - nm) : NNM_STOP_NO_ELIGIBLE;
     auto tq2 = std::chrono::steady_clock::now();
     // merge records and labels in parallel (read-only finds: the forest is final)
+    const int64_t nrec = nm - rec_from;
     const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(8, std::min<int64_t>(
-                       (int64_t)std::thread::hardware_concurrency(), (n >> 16) + 1)));
+                       (int64_t)std::thread::hardware_concurrency(),
+                       ((gpu_assign ? nrec : std::max<int64_t>(n, nrec)) >> 16) + 1)));
     auto work = [&](int t) {
-      const int64_t m0 = nm * t / nt, m1 = nm * (t + 1) / nt;
+      const int64_t m0 = rec_from + nrec * t / nt, m1 = rec_from + nrec * (t + 1) / nt;
       for (int64_t k = m0; k < m1; ++k) {
         const ReplayEdge& e = h[k];
         nnm_merge& mg = out[k];
@@ -3589,6 +4039,7 @@ struct nnm_dataset {
         mg.point_a = e.a;
         mg.point_b = e.b;
       }
+      if (gpu_assign) return;
       const int64_t i0 = n * t / nt, i1 = n * (t + 1) / nt;
       if (AS) {
         for (int64_t i = i0; i < i1; ++i) assign[i] = AS[i];
@@ -3608,14 +4059,16 @@ struct nnm_dataset {
       work(0);
       for (auto& th : pool) th.join();
     }
+    if (pin_out) sync();  // the copy engine's records and labels
     *n_merges = nm;
     *rounds = (n > 1 && stop_of(n) == 0) ? bv_round : 0;
     *stop = reason;
     if (getenv("NNM_DEBUG"))
-      fprintf(stderr, "[nnm] replay: device %.1f ms, host loop %.1f ms, records %.1f ms\n",
+      fprintf(stderr, "[nnm] replay: device %.1f ms, host loop %.1f ms, records %.1f ms%s\n",
               std::chrono::duration<double, std::milli>(tq1 - tq0).count(),
               std::chrono::duration<double, std::milli>(tq2 - tq1).count(),
-              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq2).count());
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq2).count(),
+              pin_out ? " (page-locked outputs)" : "");
   }
 
   // ---------------------------------------------------------------- top-P
@@ -3855,6 +4308,32 @@ int nnm_device_count(int32_t* out) {
   });
 }
 
+int nnm_host_alloc(int64_t bytes, void** out) {
+  return guarded([&] {
+    if (!out || bytes < 0) invalid("bad argument");
+    size_t b = (size_t)std::max<int64_t>(bytes, 1);
+    void* p = pinned_pool().get(b);
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    g_host_blocks[p] = b;
+    *out = p;
+  });
+}
+
+int nnm_host_free(void* p) {
+  return guarded([&] {
+    if (!p) return;
+    size_t b = 0;
+    {
+      std::lock_guard<std::mutex> lk(g_host_mu);
+      auto it = g_host_blocks.find(p);
+      if (it == g_host_blocks.end()) invalid("not a block from nnm_host_alloc");
+      b = it->second;
+      g_host_blocks.erase(it);
+    }
+    pinned_pool().put(p, b);
+  });
+}
+
 int nnm_dataset_create(const double* X, int64_t n, int32_t d, int32_t device, nnm_dataset** out) {
   return guarded([&] {
     if (!X || !out) invalid("null argument");
@@ -4009,7 +4488,7 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       // the caller's output arrays are usually fresh pages: fault them in on host threads
       // while the GPU rounds run, so the replay below writes to resident memory
       std::vector<std::thread> prefault;
-      if (n > 4096) {
+      if (n > 4096 && !(is_page_locked(out_merges) && is_page_locked(out_assign))) {
         char* pm = reinterpret_cast<char*>(out_merges);
         const size_t bm = (size_t)(n - 1) * sizeof(nnm_merge), half = bm / 2;
         prefault.emplace_back([pm, half] { memset(pm, 0, half); });
@@ -4028,14 +4507,20 @@ int nnm_run(nnm_dataset* ds, int32_t metric, const nnm_constraints* cons, int64_
       // -- every cross pair in FP64 every round, no screening, no pruning: an independent
       // algorithm the tests run beside the default path (at C1 it is not faster: 3.6 vs
       // 2.8 ms, FP64 row minima dominate)
+      // small inputs (n <= SMALL_AUTO_N, d <= 16) by default: the screened single-launch
+      // Boruvka (small_screened_kernel); NNM_SMALL=0 general path, 1 dense FP64, 2 screened
       const char* sme = getenv("NNM_SMALL");
-      const bool small = n > 1 && n <= 65536 && ds->d <= 16 && sme && sme[0] == '1';
+      const int small_mode = sme ? (sme[0] == '1' ? 1 : sme[0] == '2' ? 2 : 0)
+                                 : (n <= SMALL_AUTO_N ? 2 : 0);
+      bool small = n > 1 && n <= 65536 && ds->d <= 16 && small_mode > 0;
+      const bool need_s = !(cons->kl1 > 0 && n <= cons->kl1);
+      if (small && need_s) {
+        NvtxRange nv("nnm single-launch boruvka (small input)");
+        small = ds->small_boruvka(metric, cons->dmax, small_mode == 2);
+      }
       if (small) {
-        NvtxRange nv("nnm dense exact boruvka (small input)");
-        bool need_s = !(cons->kl1 > 0 && n <= cons->kl1);
         ds->stats.prep_ms = 0.0;
-        if (need_s && !ds->small_boruvka(metric, cons->dmax)) need_s = false;
-        if (!need_s) {  // nothing to merge (or no device slot): an empty edge list
+        if (!need_s) {  // nothing to merge: an empty edge list
           ds->edges.ensure(1);
           ds->counters.ensure(8);
           CUDA_TRY(cudaMemsetAsync(ds->counters.p, 0, sizeof(unsigned long long), ds->st));

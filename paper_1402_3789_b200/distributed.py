@@ -172,8 +172,8 @@ class LibBackend:
 
     def end(self, kl1):
         n = self.dd.n
-        merges = np.zeros(max(n - 1, 1), dtype=self.nat.MERGE_DTYPE)
-        assign = np.empty(n, np.int64)
+        merges = self.nat.host_empty(max(n - 1, 1), self.nat.MERGE_DTYPE)
+        assign = self.nat.host_empty(n, np.int64)
         nm, rounds = ctypes.c_int64(), ctypes.c_int64()
         stop = ctypes.c_int32()
         st = self.nat.Stats()

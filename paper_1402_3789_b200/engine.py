@@ -161,8 +161,8 @@ def run_arrays(ddata, constraints: ConstraintSet, P: int, metric: MetricKind,
     """
     n = ddata.n
     lib = _native.load()
-    merges = np.zeros(max(n - 1, 1), dtype=_native.MERGE_DTYPE)
-    assign = np.empty(n, np.int64)
+    merges = _native.host_empty(max(n - 1, 1), _native.MERGE_DTYPE)
+    assign = _native.host_empty(n, np.int64)
     ccap = n + 1
     counters = np.zeros(ccap, dtype=_native.COUNTER_DTYPE)
     nm, rounds, nc = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
@@ -201,8 +201,8 @@ def run_arrays_multi(dds, constraints: ConstraintSet, P: int, metric: MetricKind
         return run_arrays(dds[0], constraints, P, metric, exact_rounds)
     n = dds[0].n
     lib = _native.load()
-    merges = np.zeros(max(n - 1, 1), dtype=_native.MERGE_DTYPE)
-    assign = np.empty(n, np.int64)
+    merges = _native.host_empty(max(n - 1, 1), _native.MERGE_DTYPE)
+    assign = _native.host_empty(n, np.int64)
     ccap = n + 1
     counters = np.zeros(ccap, dtype=_native.COUNTER_DTYPE)
     nm, rounds, nc = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

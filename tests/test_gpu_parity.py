@@ -69,8 +69,15 @@ def test_top_p_vs_reference_golden(nnm):
         assert np.array_equal(buf.b, g[f"b_{i}"]), i
 
 
+@pytest.mark.parametrize("small", ["0", "auto"])
 @pytest.mark.parametrize("exact_rounds", [False, True])
-def test_run_vs_reference_engine_golden(nnm, exact_rounds):
+def test_run_vs_reference_engine_golden(nnm, exact_rounds, small, monkeypatch):
+    """Every reference engine case; Boruvka-eligible cases run on the general pruned path
+    (NNM_SMALL=0) and on the default selection (small inputs: the screened single launch)."""
+    if small == "auto":
+        monkeypatch.delenv("NNM_SMALL", raising=False)
+    else:
+        monkeypatch.setenv("NNM_SMALL", small)
     g = golden("run_cases.npz")
     for i in range(int(g["count"])):
         kl1, kl2, kl3, kl4, P = (int(v) for v in g[f"cons_{i}"])
@@ -96,10 +103,11 @@ def test_run_vs_reference_engine_golden(nnm, exact_rounds):
             assert np.array_equal(rc, g[f"counters_{i}"]), i
 
 
-@pytest.mark.parametrize("small", ["0", "1"])
+@pytest.mark.parametrize("small", ["0", "1", "2"])
 def test_c1_full_run_vs_reference(nnm, small, monkeypatch):
     """BASELINE config 1: 10k x 8, 5 blobs, unconstrained, P=256 (reference run here), on
-    the general pruned path and on the dense small-input path (the default for C1)."""
+    the general pruned path (0), the dense FP64 single launch (1) and the screened single
+    launch (2, the default for C1)."""
     from paper_1402_3789_b200.datagen import config_dataset
 
     monkeypatch.setenv("NNM_SMALL", small)
@@ -143,7 +151,7 @@ def test_c2_analogue_rounds_vs_reference(nnm):
     assert np.array_equal(res.assignments, g["assign"])
 
 
-@pytest.mark.parametrize("small", ["0", "1"])  # general pruned path / dense small-input path
+@pytest.mark.parametrize("small", ["0", "1", "2"])  # general pruned path / dense small-input path
 @pytest.mark.parametrize("metric", ["euclidean", "squared-euclidean", "manhattan", "chebyshev"])
 @pytest.mark.parametrize("kind", ["blobs", "ties", "dups"])
 def test_boruvka_vs_oracle_flat(nnm, metric, kind, small, monkeypatch):
@@ -240,7 +248,7 @@ def test_multi_replica_run_equals_single(nnm, replicas, kw, monkeypatch):
     assert multi.device_stats["pairs_evaluated"] == single.device_stats["pairs_evaluated"]
 
 
-@pytest.mark.parametrize("small", ["0", "1"])
+@pytest.mark.parametrize("small", ["0", "1", "2"])
 @pytest.mark.parametrize("n", [1, 2, 3, 127, 129, 300, 2049])
 def test_boruvka_small_and_ragged_sizes(nnm, n, small, monkeypatch):
     monkeypatch.setenv("NNM_SMALL", small)
@@ -258,7 +266,7 @@ def test_boruvka_small_and_ragged_sizes(nnm, n, small, monkeypatch):
         assert np.array_equal(res.assignments, a_or)
 
 
-@pytest.mark.parametrize("small", ["0", "1"])
+@pytest.mark.parametrize("small", ["0", "1", "2"])
 def test_boruvka_shuffled_blobs_vs_oracle(nnm, small, monkeypatch):
     """Row-shuffled blob data (SURVEY 8d asks for a shuffled variant): kd order + pruning
     (general path) and the dense small-input path."""

@@ -24,6 +24,13 @@ from nnm_testutil import ROOT
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _general_path(monkeypatch):
+    """These tests exercise the tile / tensor-core path: keep small inputs off the
+    single-launch small-input kernel."""
+    monkeypatch.setenv("NNM_SMALL", "0")
+
 FIELDS = ("root_a", "root_b", "dist", "new_size", "point_a", "point_b")
 
 
