@@ -276,7 +276,17 @@ __global__ void norms_kernel(const double* __restrict__ X64, int64_t n, int d, i
     s = s * (1.0 + 1e-12) + 1e-300;
   }
   norm[i] = s;
-  atomicMax(maxbits, dbits(s));
+  // one atomic per warp (2M same-address atomics serialise at the L2)
+  unsigned long long m = dbits(s);
+  if (__activemask() != 0xFFFFFFFFu) {  // the ragged last warp: one atomic per row
+    atomicMax(maxbits, m);
+    return;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long q = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+    m = q > m ? q : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(maxbits, m);
 }
 
 template <int M>
@@ -1941,21 +1951,32 @@ __global__ void kd_dim_kernel(const double* __restrict__ X64, int d, const int* 
     return;
   }
   const int b = sbeg[sgm];
-  // sample up to 64 evenly spaced points; spread per dimension
-  __shared__ float best[32];
-  __shared__ int bestk[32];
+  // sample up to 64 evenly spaced points (two per lane, rows read whole and in parallel);
+  // spread per dimension
+  const int ns = sz < 64 ? sz : 64;
+  const int lane = threadIdx.x;
+  const int t0 = lane, t1 = lane + 32;
+  const double* r0 = t0 < ns ? X64 + (int64_t)order[b + (int)((long long)t0 * sz / ns)] * d : nullptr;
+  const double* r1 = t1 < ns ? X64 + (int64_t)order[b + (int)((long long)t1 * sz / ns)] * d : nullptr;
   float bs = -1.f;
   int bk = 0;
-  for (int k = threadIdx.x; k < d; k += blockDim.x) {
+  for (int k = 0; k < d; ++k) {
     float lo = INFINITY, hi = -INFINITY;
-    const int ns = sz < 64 ? sz : 64;
-    for (int t = 0; t < ns; ++t) {
-      const int p = b + (int)((long long)t * sz / ns);
-      const float v = (float)X64[(int64_t)order[p] * d + k];
+    if (r0) {
+      const float v = (float)r0[k];
       lo = fminf(lo, v);
       hi = fmaxf(hi, v);
     }
-    if (hi - lo > bs) {
+    if (r1) {
+      const float v = (float)r1[k];
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+    }
+    if (hi - lo > bs) {  // lane-uniform after the reduction
       bs = hi - lo;
       bk = k;
     }
