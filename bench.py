@@ -440,6 +440,13 @@ def run_gpu(args) -> None:
     else:
         tr = _load_traffic(args.config)
         kname = tr["kernel"] if tr else "scan_reg_kernel"
+        kdesc = (f"{kname} (fused FP32 distance + eligibility (components, dmax, kl2/kl3 sizes) + "
+                 "per-row top-1/top-2 threshold filter)")
+        if kname == "small_screened_kernel":
+            kdesc = ("small_screened_kernel (small inputs: ONE cooperative launch for every "
+                     "Boruvka round -- FP32 screened row top-2 with packed FFMA2, FP64 "
+                     "certification, component minima, hooking, relabelling; its time includes "
+                     "the grid barriers of all rounds)")
         roofline = {"bound": "fp32", "achieved": alg_tflops, "peak": peak.value, "unit": "TFLOP/s",
                     "frac": alg_tflops / peak.value if peak.value else None,
                     "traffic": tr["dram_bytes_per_launch"] if tr else None,
@@ -447,8 +454,7 @@ def run_gpu(args) -> None:
                                      f"averaged over the {tr['launches']} launches of one "
                                      f"{args.config} device step (profiles/r2_traffic.json)")
                                     if tr else None,
-                    "kernel": f"{kname} (fused FP32 distance + eligibility (components, dmax, "
-                              "kl2/kl3 sizes) + per-row top-1/top-2 threshold filter)",
+                    "kernel": kdesc,
                     "peak_source": "measured FFMA2 microbenchmark on this GPU (MEASURED_PEAKS.json "
                                    "has no FP32 entry)",
                     "avg_launch_ms": avg_launch_ms, "launches": scans,

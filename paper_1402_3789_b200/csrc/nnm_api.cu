@@ -1870,24 +1870,36 @@ __global__ void enum_append_kernel(const unsigned* __restrict__ bnd, const int2*
   const int2 tI = trange[I];
   const double uI = umax[I];
   const int lane = threadIdx.x & 31;
-  for (int J0 = I; J0 < T; J0 += blockDim.x) {
-    const int J = J0 + threadIdx.x;
-    bool k = false;
-    if (J < T) {
-      const int64_t w = w0 + (J - I);
-      const int2 tJ = trange[J];
-      k = !((bits[w >> 5] >> (w & 31)) & 1u) &&
-          !(tI.x == tI.y && tJ.x == tJ.y && tI.x == tJ.x);  // same_single(I, J)
-      if (k && J != I) k = !((double)__uint_as_float(bnd[w]) > fmax(uI, umax[J]));
+  constexpr int U = 4;  // four independent column loads in flight per thread
+  for (int J0 = I; J0 < T; J0 += U * blockDim.x) {
+    bool k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int J = J0 + u * blockDim.x + threadIdx.x;
+      k[u] = false;
+      if (J < T) {
+        const int64_t w = w0 + (J - I);
+        const int2 tJ = trange[J];
+        const unsigned bw = bits[w >> 5];
+        const float b = __uint_as_float(bnd[w]);
+        const double uJ = umax[J];
+        k[u] = !((bw >> (w & 31)) & 1u) &&
+               !(tI.x == tI.y && tJ.x == tJ.y && tI.x == tJ.x);  // same_single(I, J)
+        if (J != I) k[u] = k[u] && !((double)b > fmax(uI, uJ));
+      }
     }
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, k);
-    if (!m) continue;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    if (k) {
-      const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
-      if (at < cap) out[at] = ((unsigned long long)I << 32) | (unsigned)J;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, k[u]);
+      if (!m) continue;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xFFFFFFFFu, base, 0);
+      if (k[u]) {
+        const int J = J0 + u * blockDim.x + threadIdx.x;
+        const unsigned long long at = base + __popc(m & ((1u << lane) - 1u));
+        if (at < cap) out[at] = ((unsigned long long)I << 32) | (unsigned)J;
+      }
     }
   }
 }

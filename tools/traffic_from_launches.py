@@ -13,7 +13,8 @@ import sys
 SCALE_T = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0,
            "s": 1e3, "second": 1e3}
 SCALE_B = {"byte": 1.0, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 1e9, "GB": 1e9}
-SCANS = ("tc_scan_kernel", "scan_reg_kernel", "scan_ws_kernel", "scan_rows_kernel", "collect_kernel")
+SCANS = ("tc_scan_kernel", "scan_reg_kernel", "scan_ws_kernel", "scan_rows_kernel", "collect_kernel",
+         "small_screened_kernel", "small_boruvka_kernel")
 
 
 def summarize(path):
