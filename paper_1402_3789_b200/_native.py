@@ -163,7 +163,7 @@ def first_nonfinite(values: np.ndarray) -> int:
     return int(out.value)
 
 
-HOST_OUT_MIN = 1 << 22        # smaller outputs stay ordinary numpy arrays
+HOST_OUT_MIN = 1 << 20        # smaller outputs stay ordinary numpy arrays
 HOST_OUT_CAP = 8 << 30        # page-locked output bytes alive at once (then ordinary arrays)
 _host_out = 0
 
