@@ -4269,6 +4269,61 @@ void init_device(int32_t device, int* sms) {
   }
 }
 
+// Host -> device copy of a large PAGEABLE array: the driver would stage it through a small
+// bounce buffer at a fraction of the link rate.  Here T host threads copy slices into
+// page-locked double buffers (pinned_pool) and each queues the DMA of its buffer on `st`,
+// so the host copies overlap the transfers.  Page-locked sources go straight to the DMA.
+void upload_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  constexpr size_t kChunk = (size_t)8 << 20;
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  if (bytes < ((size_t)32 << 20) || is_page_locked(src)) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    return;
+  }
+  const int T = std::max(1, std::min(8, hw / 2));
+  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  std::vector<std::thread> pool;
+  std::atomic<int> failed{0};
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  for (int t = 0; t < T; ++t) {
+    pool.emplace_back([&, t] {
+      cudaSetDevice(dev);
+      void* buf[2] = {nullptr, nullptr};
+      size_t bb[2] = {kChunk, kChunk};
+      cudaEvent_t ev[2] = {nullptr, nullptr};
+      bool used[2] = {false, false};
+      try {
+        for (int b = 0; b < 2; ++b) {
+          buf[b] = pinned_pool().get(bb[b]);
+          if (cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming) != cudaSuccess) throw 0;
+        }
+        int k = 0;
+        for (size_t c = (size_t)t; c < nchunks; c += (size_t)T, k ^= 1) {
+          const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+          if (used[k] && cudaEventSynchronize(ev[k]) != cudaSuccess) throw 0;
+          memcpy(buf[k], (const char*)src + off, len);
+          if (cudaMemcpyAsync((char*)dst + off, buf[k], len, cudaMemcpyHostToDevice, st) !=
+                  cudaSuccess ||
+              cudaEventRecord(ev[k], st) != cudaSuccess)
+            throw 0;
+          used[k] = true;
+        }
+        for (int b = 0; b < 2; ++b)
+          if (used[b]) cudaEventSynchronize(ev[b]);
+      } catch (...) {
+        failed.store(1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        if (ev[b]) cudaEventDestroy(ev[b]);
+        if (buf[b]) pinned_pool().put(buf[b], bb[b]);
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
+  if (failed.load()) throw NnmError{NNM_E_CUDA, "staged host-to-device upload failed"};
+}
+
 nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d, int32_t device) {
   if (n < 1 || d < 1)
     invalid("dataset must have at least 1 point and 1 feature, got " + std::to_string(n) + "x" +
@@ -4295,8 +4350,11 @@ nnm_dataset* make_dataset(const double* X, bool on_device, int64_t n, int32_t d,
       throw NnmError{NNM_E_UNSUPPORTED, "d too large for the shared-memory tile (d <= 190)"};
     auto tc0 = std::chrono::steady_clock::now();
     ds->X64.ensure((size_t)n * d);
-    CUDA_TRY(cudaMemcpyAsync(ds->X64.p, X, (size_t)n * d * sizeof(double),
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ds->st));
+    if (on_device)
+      CUDA_TRY(cudaMemcpyAsync(ds->X64.p, X, (size_t)n * d * sizeof(double),
+                               cudaMemcpyDeviceToDevice, ds->st));
+    else
+      upload_h2d(ds->X64.p, X, (size_t)n * d * sizeof(double), ds->st);
     ds->X32.ensure((size_t)ds->ld * d);
     ds->flag.ensure(1);  // scratch flag of the view build / pointer jumping
     DevBuf<unsigned long long> chk;
