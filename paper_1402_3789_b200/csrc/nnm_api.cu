@@ -2739,6 +2739,10 @@ struct nnm_dataset {
     a.dot_center = nullptr;
     a.dot_B = a.dot_nbk = a.dot_Bmax = nullptr;
     a.dot_k = a.dot_onepA = 1.f;
+    a.tpmin = nullptr;
+    a.em = em;
+    a.rsum = 2.0 * maxnorm * (1.0 + 1e-12);
+    if (tpmin_use && items && cur_X32 == X32p.p && !(dot_on && cur_X32 == X32p.p)) a.tpmin = tpmin.p;
     if (dot_on && cur_X32 == X32p.p) {
       a.dot_center = tcenter32.p;
       a.dot_B = dotB.p;
@@ -3082,7 +3086,9 @@ struct nnm_dataset {
     // tile-pair bound cache (TC scan only; 4 B per tile pair: 0.58 GB at 2M points)
     const char* ce = getenv("NNM_TPCACHE");
     tpmin_use = false;
-    tpmin_on = tc_on && !(ce && ce[0] == '0') && tile_pairs() * 4 <= ((int64_t)4 << 30);
+    // the tensor-core scan and the direct-form FP32 scans (L1 / L-inf) both publish it
+    tpmin_on = (tc_on || metric == MANHATTAN || metric == CHEBYSHEV) && !(ce && ce[0] == '0') &&
+               tile_pairs() * 4 <= ((int64_t)4 << 30);
     if (tpmin_on) {
       tpmin.ensure(tile_pairs());
       // the cache starts from the geometric bounds (both are lower bounds of every pair)

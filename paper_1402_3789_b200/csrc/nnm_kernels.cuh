@@ -29,6 +29,12 @@ struct ScanArgs {
   const float* dot_Bmax;    // [T] max B over the tile, rounded up
   float dot_k;              // 1/(1+A) rounded down
   float dot_onepA;          // 1+A rounded up
+  // tile-pair cache (direct form, scan_reg_kernel; nullptr: off): every item publishes
+  // exact_lower(min of its screened values) with atomicMax -- a rigorous lower bound of
+  // every pair of the tile pair, valid in every later round (DESIGN 3.1)
+  unsigned* tpmin;
+  ErrModel em;    // the screen's error model
+  double rsum;    // bound on norm(x) + norm(y) over all pairs (2 x max norm)
 };
 
 struct CollectArgs {

@@ -41,6 +41,39 @@ __device__ __forceinline__ void insert_top2(unsigned long long* G1, unsigned lon
   if (key_valid(m)) atomicMin(G2, m);
 }
 
+// The same insert split in two so that the returning atomicMin's latency overlaps the next
+// item's arithmetic: start() issues the G1 atomic and keeps (k1, k2, old); finish() -- at the
+// thread's next start() or at the end of the kernel -- derives the displaced key and issues
+// the (non-returning) G2 atomic.  The protocol stays order independent (each displacement
+// is decided by the atomic's return value); other readers of G2 in between only see a
+// looser (larger) second-best key, which is safe for thresholds.
+struct Top2Flush {
+  bool pend = false;
+  unsigned long long* g2 = nullptr;
+  unsigned long long k1 = 0, k2 = 0, old = 0;
+  __device__ __forceinline__ void finish() {
+    if (!pend) return;
+    pend = false;
+    const unsigned long long disp = (k1 < old) ? old : k1;
+    const unsigned long long m = disp < k2 ? disp : k2;
+    if (key_valid(m)) atomicMin(g2, m);
+  }
+  __device__ __forceinline__ void start(unsigned long long* G1, unsigned long long* G2,
+                                        unsigned long long a1, unsigned long long a2) {
+    finish();
+    if (!key_valid(a1)) return;
+    if (G2 == nullptr) {
+      atomicMin(G1, a1);
+      return;
+    }
+    old = atomicMin(G1, a1);
+    k1 = a1;
+    k2 = a2;
+    g2 = G2;
+    pend = true;
+  }
+};
+
 __device__ __forceinline__ void decode_work(int64_t w, int T, int& I, int& J) {
   // start(I) = I*T - I*(I-1)/2 ; find the largest I with start(I) <= w
   double tt = 2.0 * T + 1.0;
@@ -287,6 +320,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
   const int64_t w0 = p.w_begin + (int64_t)blockIdx.x * per;
   const int64_t w1 = min(w0 + per, p.w_end);
   if (w0 >= w1) return;
+  Top2Flush gflush;  // this thread's pending global top-2 insert
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -443,7 +477,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
       const bool flush = !has_next || In != I;
       if (flush) {
         const int g = I * TILE + tid;
-        if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, a1, a2);
+        if (g < p.n) gflush.start(p.B1 + g, TOP2 ? p.B2 + g : nullptr, a1, a2);
         a1 = NONE_KEY;
         a2 = NONE_KEY;
       }
@@ -455,7 +489,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
 #pragma unroll
       for (int q = 1; q < 4; ++q) merge2(a1, a2, colPart[2 * (q * TILE + c)], colPart[2 * (q * TILE + c) + 1]);
       const int g = J * TILE + c;
-      if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, a1, a2);
+      if (g < p.n) gflush.start(p.B1 + g, TOP2 ? p.B2 + g : nullptr, a1, a2);
     }
     if (has_next && In != I) {
       async_tile(sX, sCompR, sSizeR, p.X32, p.ld, In, p.d, p.comp, p.psize, SIZES);
@@ -467,6 +501,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_rows_kernel(ScanArgs p) 
     J = Jn;
     buf ^= 1;
   }
+  gflush.finish();
 }
 
 size_t scan_smem_bytes(int d) {
@@ -567,6 +602,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
   const int64_t w0 = p.w_begin + (int64_t)blockIdx.x * per;
   const int64_t w1 = min(w0 + per, p.w_end);
   if (w0 >= w1) return;
+  Top2Flush gflush;  // this thread's pending global top-2 insert
   const int tid = threadIdx.x;
   int I, J;
   first_item(p, w0, I, J);
@@ -863,18 +899,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1) scan_ws_kernel(ScanArgs p) {
       if (is_row) {
         if (w + 1 >= w1 || In != I) {
           const int g = I * TILE + t;
-          if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, run1, run2);
+          if (g < p.n) gflush.start(p.B1 + g, TOP2 ? p.B2 + g : nullptr, run1, run2);
           run1 = NONE_KEY;
           run2 = NONE_KEY;
         }
       } else if (!diag) {
         const int g = J * TILE + t;
-        if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, k1, k2);
+        if (g < p.n) gflush.start(p.B1 + g, TOP2 ? p.B2 + g : nullptr, k1, k2);
       }
       I = In;
       J = Jn;
     }
   }
+  gflush.finish();
 }
 
 size_t scan_ws_smem_bytes(int d) {
@@ -913,12 +950,14 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
   int* sSC = sSR + 2 * TILE;                            // [2 buf][128]
   uint32_t* sGR = reinterpret_cast<uint32_t*>(sSC + 2 * TILE);  // [2 xb][128] global row d-parts
   uint32_t* sGC = sGR + 2 * TILE;                               // [2 buf][128] global col d-parts
+  __shared__ unsigned sTmin[2];  // per buffer: min screened value of the item (bits)
 
   const int64_t total = p.w_end - p.w_begin;
   const int64_t per = (total + gridDim.x - 1) / gridDim.x;
   const int64_t w0 = p.w_begin + (int64_t)blockIdx.x * per;
   const int64_t w1 = min(w0 + per, p.w_end);
   if (w0 >= w1) return;
+  Top2Flush gflush;  // this thread's pending global top-2 insert
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -935,6 +974,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
   async_tile(sY0, sCC, sSC, p.X32, p.ld, J, p.d, p.comp, p.psize, SIZES);
   cp_async_commit();
   for (int t = tid; t < 8 * TILE; t += SCAN_THREADS) rowTop[t] = NONE_KEY;  // rowTop + colTop
+  if (tid < 2) sTmin[tid] = 0xFFFFFFFFu;
   int xb = 0;
   bool xfresh = true;
   int prevI = -1, prevJ = -1, prevBuf = 0, prevXb = 0;
@@ -943,12 +983,24 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
     cp_async_wait_all();
     __syncthreads();  // (A) tiles of w resident; inserts of w-1 complete
     // ---- flush the previous item's column slots, and its row slots if I changes
+    if (!DOT && p.tpmin && prevJ >= 0 && tid == SCAN_THREADS - 1) {
+      // the previous item's tile-pair bound (every warp's minimum has landed: barrier A)
+      const unsigned mb = sTmin[prevBuf];
+      sTmin[prevBuf] = 0xFFFFFFFFu;
+      const float v = __uint_as_float(mb);
+      if (mb < 0x7F800000u) {
+        const float L = float_down(exact_lower(p.em, (double)v, p.rsum));
+        const int lo = min(prevI, prevJ), hi = max(prevI, prevJ);
+        const int64_t wi = (int64_t)lo * p.T - (int64_t)lo * (lo - 1) / 2 + (hi - lo);
+        if (L > 0.f) atomicMax(p.tpmin + wi, __float_as_uint(L));
+      }
+    }
     if (prevJ >= 0) {
       if (tid < TILE) {
         if (prevI != prevJ) {
           unsigned long long* ct = colTop + prevBuf * 2 * TILE;
           const int g = prevJ * TILE + tid;
-          if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, ct[tid], ct[TILE + tid]);
+          if (g < p.n) gflush.start(p.B1 + g, TOP2 ? p.B2 + g : nullptr, ct[tid], ct[TILE + tid]);
           ct[tid] = NONE_KEY;
           ct[TILE + tid] = NONE_KEY;
         }
@@ -956,7 +1008,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
         const int r = tid - TILE;
         unsigned long long* rt = rowTop + prevXb * 2 * TILE;
         const int g = prevI * TILE + r;
-        if (g < p.n) insert_top2(p.B1 + g, TOP2 ? p.B2 + g : nullptr, rt[r], rt[TILE + r]);
+        if (g < p.n) gflush.start(p.B1 + g, TOP2 ? p.B2 + g : nullptr, rt[r], rt[TILE + r]);
         rt[r] = NONE_KEY;
         rt[TILE + r] = NONE_KEY;
       }
@@ -1062,6 +1114,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
     // ---- filter: any value at or below its row or column threshold?  (dot form:
     // v = -2 acc, so v <= t  <=>  acc >= -t/2, an exact rescaling)
     bool hit = false;
+    float tmin = INFINITY;  // smallest screened value of this thread's pairs (direct form)
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       if (DOT) {
@@ -1072,7 +1125,15 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
         const float m = fminf(fminf(fminf(acc[r][0].x, acc[r][0].y), fminf(acc[r][1].x, acc[r][1].y)),
                               fminf(fminf(acc[r][2].x, acc[r][2].y), fminf(acc[r][3].x, acc[r][3].y)));
         hit |= m <= tR[r];
+        tmin = fminf(tmin, m);
       }
+    }
+    if (!DOT && p.tpmin) {
+      // pads give +inf (or NaN for pad x pad, dropped by fminf); same-component pairs are
+      // included -- a min over a superset, still a lower bound for the cross pairs
+      const unsigned tb = tmin >= 0.f ? __float_as_uint(tmin) : 0u;
+      const unsigned wmin = __reduce_min_sync(0xFFFFFFFFu, tmin == tmin ? tb : 0xFFFFFFFFu);
+      if (lane == 0) atomicMin(&sTmin[buf], wmin);
     }
     if (!diag) {
 #pragma unroll
@@ -1091,12 +1152,15 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
         const int R = row0 + r;
         const int cR = sCR[xb * TILE + R];
         const int sRv = SIZES ? sSR[xb * TILE + R] : 0;
+        // the row's best two among this thread's 8 columns first: one shared insert per row
+        // instead of one per column (rows start with no threshold in a fresh row tile)
+        unsigned long long b1 = NONE_KEY, b2 = NONE_KEY;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int C = colw + wcol(tc, c);
           const float v = DOT ? -2.f * acc_at(acc, r, c) : acc_at(acc, r, c);
           const bool prow = v <= tR[r];
-          const bool pcol = !diag && v <= tC[c];
+          bool pcol = !diag && v <= tC[c];
           if (!(prow || pcol)) continue;
           const int cC = sCC[buf * TILE + C];
           bool ok = cR != cC && cR >= 0 && cC >= 0 && fabsf(v) < INFINITY;
@@ -1105,14 +1169,26 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
           if (THR) ok = ok && (L <= p.thr_hi);
           if (!ok) continue;
           const unsigned long long dp = (unsigned long long)__float_as_uint(L) << 32;
-          if (prow)
-            insert_top2(const_cast<unsigned long long*>(rt) + R,
-                        TOP2 ? const_cast<unsigned long long*>(rt) + TILE + R : nullptr,
-                        dp | (unsigned long long)(J * TILE + C), NONE_KEY);
-          if (pcol)
-            insert_top2(ct + C, TOP2 ? ct + TILE + C : nullptr,
-                        dp | (unsigned long long)(I * TILE + R), NONE_KEY);
+          if (prow) {
+            const unsigned long long key = dp | (unsigned long long)(J * TILE + C);
+            if (key < b1) {
+              b2 = b1;
+              b1 = key;
+            } else if (key < b2) {
+              b2 = key;
+            }
+          }
+          if (pcol) {
+            const unsigned long long key = dp | (unsigned long long)(I * TILE + R);
+            // skip the atomic when the column's current slot already beats the key
+            if (key < (TOP2 ? ct[TILE + C] : ct[C]))
+              insert_top2(ct + C, TOP2 ? ct + TILE + C : nullptr, key, NONE_KEY);
+          }
         }
+        if (key_valid(b1))
+          insert_top2(const_cast<unsigned long long*>(rt) + R,
+                      TOP2 ? const_cast<unsigned long long*>(rt) + TILE + R : nullptr, b1,
+                      TOP2 ? b2 : NONE_KEY);
       }
     }
     prevI = I;
@@ -1126,6 +1202,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 2) scan_reg_kernel(ScanArgs p) {
     I = In;
     J = Jn;
   }
+  gflush.finish();
 }
 
 size_t scan_reg_smem_bytes(int d) {
