@@ -2309,6 +2309,13 @@ __global__ void active_rows_kernel(int n, const unsigned long long* __restrict__
   }
 }
 
+// candidate distances rounded UP to fp32 (a monotone map: the P-th smallest of these is
+// an upper bound of the P-th smallest distance) as radix-sortable keys
+__global__ void cand_keys_kernel(const Cand* __restrict__ c, int64_t n, float* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = float_up(c[t].d);
+}
+
 __global__ void pairs_to_cands_kernel(const int2* __restrict__ pairs, const double* __restrict__ dv,
                                       int64_t count, double lim, Cand* out,
                                       unsigned long long* n_out) {
@@ -2582,6 +2589,8 @@ struct nnm_dataset {
   const int2* p1_list = nullptr;
   // round path
   DevBuf<Cand> cands, cands2;
+  DevBuf<float> ckeys, ckeys2;  // tau selection keys (top_p_pass)
+  DevBuf<char> ctmp;
   DevBuf<unsigned long long> rB1;  // round path: per-row best screened key (may be stale)
   bool rb1_valid = false;
   DevBuf<int> active, rmap, rsize;
@@ -4143,9 +4152,16 @@ struct nnm_dataset {
     stats.exact_evals += nc;
     double tau = INFINITY;
     if (nc >= P) {
-      thrust::sort(thrust::cuda::par(talloc).on(st), cands.p, cands.p + nc, CandLess());
-      Cand c = read1(cands.p + (P - 1));
-      tau = c.d;
+      // tau = the P-th smallest candidate distance, rounded up to fp32: a radix sort of
+      // 32-bit keys instead of a merge sort of the 16-byte candidates
+      ckeys.ensure(nc);
+      ckeys2.ensure(nc);
+      cand_keys_kernel<<<blocks_for(nc), 256, 0, st>>>(cands.p, nc, ckeys.p); note_launch();
+      size_t tb = 0;
+      CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tb, ckeys.p, ckeys2.p, (int)nc, 0, 32, st));
+      ctmp.ensure(std::max<size_t>(tb, 1));
+      CUDA_TRY(cub::DeviceRadixSort::SortKeys(ctmp.p, tb, ckeys.p, ckeys2.p, (int)nc, 0, 32, st));
+      tau = (double)read1(ckeys2.p + (P - 1));
     } else if (max_active < n) {
       return false;  // too few surviving row-best pairs: rescan
     }
