@@ -2564,6 +2564,8 @@ struct nnm_dataset {
   DevBuf<unsigned> ucap;        // this rank's caps from its bound-pass share (u32 fp32 bits)
   DevBuf<unsigned> capp;        // per position: its component's cap (staged by the scan)
   DevBuf<int> tc_slots;         // [Tp][16] per-round slot records (tc_tails)
+  DevBuf<unsigned long long> tc_cand;  // deferred exact-key candidates (tc_launch)
+  bool tc_phase2 = false;              // the current tc_scan is a phase-2 pass
   int64_t tc_tails_epoch = -1;  // scan_epoch the A tails / slot records were written for
 
   // A-side tails of the operand image and the slot records for the current components
@@ -2810,6 +2812,7 @@ struct nnm_dataset {
                int64_t w_end, const int2* items, const double* umax = nullptr) {
     const int64_t n_up = w_end - w_begin;
     if (n_up <= 0) return;
+    tc_phase2 = umax != nullptr;
     tc_prepare();
     tc_tails();
     // the bound pass and the exact pass of phase 1 scan the same list: mirror + sort once
@@ -2878,6 +2881,24 @@ struct nnm_dataset {
     a.slots = tc_slots.p;     // slot records + A tails of this round (tc_tails)
     const char* dbg = getenv("NNM_TC_DBG");
     a.dbg = dbg ? atoi(dbg) : 0;
+    // deferred exact keys (exact passes): candidates appended by the scan, FP64-evaluated
+    // by tc_exact_kernel right after it (NNM_TC_DEFER=0: in the epilogue)
+    const char* dfe = getenv("NNM_TC_DEFER");
+    // phase-1 passes only: there the rows' thresholds come from the bound pass / the seeds
+    // and tighten little within a launch; phase-2 rows tighten as exact keys arrive, and
+    // deferring them would multiply the candidates (C4 round 1: 1.5 -> 6.3 ms)
+    const bool defer = !tc_bound_only && !tc_phase2 && !(dfe && dfe[0] == '0');
+    a.cand = nullptr;
+    a.ccount = nullptr;
+    a.ccap = 0;
+    if (defer) {
+      tc_cand.ensure((size_t)1 << 24);
+      counters.ensure(8);
+      CUDA_TRY(cudaMemsetAsync(counters.p + 7, 0, sizeof(unsigned long long), st));
+      a.cand = tc_cand.p;
+      a.ccount = counters.p + 7;
+      a.ccap = tc_cand.n;
+    }
     const int grid = (int)std::min<int64_t>(nfull, (int64_t)sms);
     const char* trf = getenv("NNM_TC_TRACE");
     DevBuf<long long> trbuf;
@@ -2890,6 +2911,13 @@ struct nnm_dataset {
     scan_timer_start();
     CUDA_TRY(launch_tc_scan(a, grid, st));
     note_launch();
+    if (a.cand) {
+      CUDA_TRY(launch_tc_exact(a.cand, a.ccount, (int64_t)a.ccap, X64p.p, d, thr_hi, b1, b2, st));
+      note_launch();
+      if (getenv("NNM_DEBUG"))
+        fprintf(stderr, "[nnm] tc deferred candidates: %llu (cap %llu)\n",
+                (unsigned long long)read1(a.ccount), (unsigned long long)a.ccap);
+    }
     scan_timer_stop();
     stats.tc_items += nfull;
     if (getenv("NNM_DEBUG")) {

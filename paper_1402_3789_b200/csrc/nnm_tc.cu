@@ -767,6 +767,18 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
             if (!(lower_key(__fmaf_rn(-2.f, w[u], r), Erow, eta_row) <= T)) continue;
             m8 |= 1u << u;
           }
+          if (p.cand && m8) {  // deferred: append, evaluated after the scan (tc_exact)
+            const unsigned nc8 = __popc(m8);
+            const unsigned long long at = atomicAdd(p.ccount, (unsigned long long)nc8);
+            if (at + nc8 <= p.ccap) {
+              unsigned long long* o = p.cand + at;
+              while (m8) {
+                const int u = __ffs(m8) - 1;
+                m8 &= m8 - 1;
+                *o++ = ((unsigned long long)g << 32) | (unsigned)((int64_t)J * TILE + gidx * 8 + u);
+              }
+            }  // else: the buffer is full -- these lanes evaluate in place below
+          }
           // lockstep: each iteration every lane evaluates its next candidate of the group
 #pragma unroll 1
           while (__any_sync(0xFFFFFFFFu, m8 != 0u)) {
@@ -1007,6 +1019,31 @@ static cudaError_t launch_tc_d(const TcArgs& a, int grid, cudaStream_t st) {
               fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, sm, fa.localSizeBytes);
   }
   return e;
+}
+
+__global__ void tc_exact_kernel(const unsigned long long* __restrict__ cand,
+                                const unsigned long long* __restrict__ count, int64_t cap,
+                                const double* __restrict__ X64, int d, float thr_hi,
+                                unsigned long long* B1, unsigned long long* B2) {
+  const int64_t n = min((int64_t)*count, cap);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long c = cand[t];
+    const int64_t g = (int64_t)(c >> 32), gj = (int64_t)(c & 0xFFFFFFFFull);
+    const float L = float_down(exact_dist<EUCLIDEAN>(X64 + g * d, X64 + gj * d, d));
+    if (!(L <= thr_hi)) continue;
+    const unsigned long long key = ((unsigned long long)__float_as_uint(L) << 32) | (unsigned)gj;
+    const unsigned long long old = atomicMin(B1 + g, key);  // atomic top-2 insert
+    const unsigned long long disp = key < old ? old : key;
+    if (key_valid(disp)) atomicMin(B2 + g, disp);
+  }
+}
+
+cudaError_t launch_tc_exact(const unsigned long long* cand, const unsigned long long* count,
+                            int64_t cap, const double* X64, int d, float thr_hi,
+                            unsigned long long* B1, unsigned long long* B2, cudaStream_t st) {
+  tc_exact_kernel<<<148 * 8, 256, 0, st>>>(cand, count, cap, X64, d, thr_hi, B1, B2);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tc_tails(float* img, const int* comp, int T, int d, int* slots, cudaStream_t st) {

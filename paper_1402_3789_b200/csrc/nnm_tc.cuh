@@ -42,9 +42,19 @@ struct TcArgs {
   const unsigned* capp;   // [np] per position: its component's cap (capped exact passes)
   const int* slots;       // [T][16] per-round slot records (launch_tc_tails)
   const int2* trange;     // [T] min / max component label per tile (nullptr: always check)
+  // deferred exact keys (nullptr: evaluate in the epilogue): candidates passing the
+  // screen are appended as (row position << 32 | column position) and evaluated by
+  // launch_tc_exact after the scan -- the FP64 gathers leave the tensor-core pipeline
+  unsigned long long* cand;
+  unsigned long long* ccount;
+  unsigned long long ccap;
 };
 
 size_t tc_smem_bytes();
+// exact keys of the deferred candidates into the rows' atomic top-2 (B1, B2)
+cudaError_t launch_tc_exact(const unsigned long long* cand, const unsigned long long* count,
+                            int64_t cap, const double* X64, int d, float thr_hi,
+                            unsigned long long* B1, unsigned long long* B2, cudaStream_t st);
 bool tc_supported(int d);
 cudaError_t launch_tc_scan(const TcArgs& a, int grid, cudaStream_t st);
 // per-round slot records + A-side operand tails for the current component labels
