@@ -155,3 +155,35 @@ def test_tile_pair_bound_cache_identical_at_full_scale(nnm, cfg):
     if cfg == "c4":
         assert a[2] == "1999999"
         assert int(a[1]) < int(b[1])
+
+
+def test_tc_deferred_and_in_epilogue_keys_identical(nnm):
+    """500k x 25 (config 3's data, no dmax): phase-1 exact keys evaluated after the scan
+    from the appended candidates (default) and inside the epilogue (NNM_TC_DEFER=0) give
+    byte-identical dendrograms."""
+    code = ("import hashlib, paper_1402_3789_b200 as nnm\n"
+            "from paper_1402_3789_b200.datagen import config_dataset\n"
+            "X = config_dataset('c3')\n"
+            "r = nnm.fit(X)\n"
+            "print(hashlib.sha256(r.merges.array.tobytes() + r.assignments.tobytes()).hexdigest(),"
+            " r.device_stats['tc_items'] > 0, len(r.merges))\n")
+    a = _run_env(code, {"NNM_TC_DEFER": "1"}).split()
+    b = _run_env(code, {"NNM_TC_DEFER": "0"}).split()
+    assert a[1] == "True" and b[1] == "True"
+    assert a[0] == b[0] and a[2] == b[2] == "499999"
+
+
+@pytest.mark.parametrize("metric", ["manhattan", "chebyshev"])
+def test_fp32_tile_pair_cache_identical(nnm, metric):
+    """500k x 25, L1 / L-inf: the FP32 direct scan's tile-pair cache (exact_lower of each
+    item's minimum) prunes later rounds without changing the dendrogram."""
+    code = ("import hashlib, paper_1402_3789_b200 as nnm\n"
+            "from paper_1402_3789_b200.datagen import config_dataset\n"
+            "X = config_dataset('c3')\n"
+            f"r = nnm.fit(X, metric='{metric}')\n"
+            "print(hashlib.sha256(r.merges.array.tobytes() + r.assignments.tobytes()).hexdigest(),"
+            " int(r.device_stats['pairs_evaluated']))\n")
+    a = _run_env(code, {"NNM_TPCACHE": "1"}).split()
+    b = _run_env(code, {"NNM_TPCACHE": "0"}).split()
+    assert a[0] == b[0]
+    assert int(a[1]) < int(b[1])
