@@ -2496,7 +2496,8 @@ struct nnm_dataset {
   DevBuf<ReplayEdge> replay;
   PinnedBuf<ReplayEdge> host_replay;
   PinnedBuf<int32_t> h_rk, h_rd, h_rs, h_as;
-  DevBuf<int> r_par, r_sz, r_lab, r_head, r_ea, r_eb, r_nxt, r_comp, r_ctl, r_rk, r_rd, r_rs;
+  DevBuf<int> r_par, r_sz, r_lab, r_head, r_ea, r_eb, r_nxt, r_comp, r_ctl, r_rk, r_rd, r_rs,
+      r_base, r_slot, r_rid, r_rcnt, r_llist;
   cudaGraphExec_t rp_exec = nullptr;  // captured replay chunk sequence (see bv_end)
   int64_t rp_m = -1, rp_n = -1, rp_nch = -1;
   int rp_lmax = -1;
@@ -3937,12 +3938,18 @@ struct nnm_dataset {
       r_eb.ensure(cmax_chunk);
       r_nxt.ensure(cmax_chunk);
       r_comp.ensure(cmax_chunk);
-      r_ctl.ensure(4);
+      r_ctl.ensure(8);
+      r_base.ensure(n);
+      r_slot.ensure(cmax_chunk);
+      r_rid.ensure(n);
+      r_rcnt.ensure(n);
+      r_llist.ensure(cmax_chunk);
       r_rk.ensure(m);
       r_rd.ensure(m);
       r_rs.ensure(m);
       ReplayState rs{r_par.p, r_sz.p, r_lab.p, r_head.p, r_ea.p, r_eb.p, r_nxt.p, r_comp.p,
-                     r_ctl.p, r_rk.p, r_rd.p, r_rs.p};
+                     r_ctl.p, r_rk.p, r_rd.p, r_rs.p, r_base.p, r_slot.p, r_rid.p, r_rcnt.p,
+                     r_llist.p};
       const int64_t nch = (int64_t)plan.size();
       const char* gre = getenv("NNM_REPLAY_GRAPH");
       const bool use_graph = !dbg && !(gre && gre[0] == '0');
@@ -3992,7 +3999,7 @@ struct nnm_dataset {
           fprintf(stderr, "\n");
         }
       }
-      g_launches.fetch_add(1 + 5 * nch, std::memory_order_relaxed);
+      g_launches.fetch_add(1 + 7 * nch, std::memory_order_relaxed);
       lap("chunks");
       int ctl[4];
       CUDA_TRY(cudaMemcpyAsync(ctl, r_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, st));

@@ -64,16 +64,23 @@ struct ReplayEdge {  // sorted MST edge for the merge replay
 
 // GPU merge replay (nnm_replay.cu): forest state + one chunk's scratch
 constexpr int REPLAY_LMAX = 128;  // longest component replayed on the GPU
+constexpr int REPLAY_SHORT = 4;   // longer components are replayed by a warp
 struct ReplayState {
   int* par;   // [n] union-find over points (roots = minimum index, model.py:148-160)
   int* sz;    // [n] cluster size at each root
   int* lab;   // [n] scratch labels for the per-chunk components
-  int* head;  // [n] per-component list heads
+  int* head;  // [n] per-component edge count of the chunk
   int *ea, *eb;       // [chunk] roots of the edge ends at chunk start
-  int *nxt, *comp;    // [chunk] list links, component label per edge
+  int *nxt, *comp;    // [chunk] position of the edge in its component, component label
   int* ctl;  // [0] stop flag, [1] first edge the host must replay (-1: none), [2] max
-             // component length seen, [3] cycle detected (internal error)
+             // component length seen, [3] cycle detected (internal error), [4] slot
+             // allocator, [5] long components listed
   int *rk, *rd, *rs;  // [m] kept root, dropped root, new size per merge
+  int* base;  // [n] first slot of each component's edge block
+  int* slot;  // [chunk] edge blocks: each component's chunk offsets, contiguous
+  int* rid;   // [n] local id of each chunk-start root within its component
+  int* rcnt;  // [n] distinct chunk-start roots per component
+  int* llist; // [chunk] owners of the components replayed by a warp (long ones)
 };
 cudaError_t replay_init(int64_t n, const ReplayState& s, cudaStream_t st);
 cudaError_t replay_chunk(const ReplayEdge* e, int64_t lo, int cnt, int lmax, const ReplayState& s,
