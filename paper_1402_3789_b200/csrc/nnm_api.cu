@@ -2498,7 +2498,8 @@ struct nnm_dataset {
   PinnedBuf<int32_t> h_rk, h_rd, h_rs, h_as;
   DevBuf<int> r_par, r_sz, r_lab, r_head, r_ea, r_eb, r_nxt, r_comp, r_ctl, r_rk, r_rd, r_rs,
       r_base, r_slot, r_rid, r_rcnt, r_llist;
-  cudaGraphExec_t rp_exec = nullptr;  // captured replay chunk sequence (see bv_end)
+  cudaGraphExec_t rp_exec = nullptr, rp_exec2 = nullptr;  // captured replay chunks (bv_end)
+  int64_t rp_split = 0;  // first chunk of the second graph
   int64_t rp_m = -1, rp_n = -1, rp_nch = -1;
   int rp_lmax = -1;
   const void* rp_e = nullptr;
@@ -2634,6 +2635,7 @@ struct nnm_dataset {
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);
     if (rp_exec) cudaGraphExecDestroy(rp_exec);
+    if (rp_exec2) cudaGraphExecDestroy(rp_exec2);
     for (auto e : tev_pool) cudaEventDestroy(e);
     if (st2) {
       cudaStreamSynchronize(st2);
@@ -3898,6 +3900,7 @@ struct nnm_dataset {
     int32_t* RS = h_rs.ensure(std::max<int64_t>(m, 1));
     int32_t* AS = nullptr;  // labels from the GPU (nullptr: host finds)
     int64_t host_from = 0;  // first merge replayed on the host
+    int64_t early_n = 0;    // records copied out while the second replay graph ran
     int64_t rec_from = 0;   // first merge record the host writes
     bool gpu_assign = false;  // labels written to `assign` by the copy engine
     replay_host_buffers();
@@ -3959,19 +3962,28 @@ struct nnm_dataset {
                           rp_e == replay.p && rp_nch == nch &&
                           memcmp(&rp_state, &rs, sizeof(rs)) == 0;
         if (!same) {
-          if (rp_exec) cudaGraphExecDestroy(rp_exec);
-          rp_exec = nullptr;
-          cudaGraph_t gr = nullptr;
-          CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-          cudaError_t ce2 = replay_init(n, rs, st);
-          for (auto& pc : plan)
-            if (ce2 == cudaSuccess) ce2 = replay_chunk(replay.p, pc.first, pc.second, lmax, rs, st);
-          const cudaError_t ce3 = cudaStreamEndCapture(st, &gr);
-          CUDA_TRY(ce2);
-          CUDA_TRY(ce3);
-          const cudaError_t ce4 = cudaGraphInstantiate(&rp_exec, gr, 0);
-          cudaGraphDestroy(gr);
-          CUDA_TRY(ce4);
+          // two graphs: the chunks before rp_split, then the rest, so that the records of
+          // the first part can be copied out while the second part runs (page-locked
+          // outputs, below)
+          for (cudaGraphExec_t* ex : {&rp_exec, &rp_exec2}) {
+            if (*ex) cudaGraphExecDestroy(*ex);
+            *ex = nullptr;
+          }
+          rp_split = nch / 2;
+          for (int part = 0; part < 2; ++part) {
+            cudaGraph_t gr = nullptr;
+            CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            cudaError_t ce2 = part == 0 ? replay_init(n, rs, st) : cudaSuccess;
+            for (int64_t c = part == 0 ? 0 : rp_split; c < (part == 0 ? rp_split : nch); ++c)
+              if (ce2 == cudaSuccess)
+                ce2 = replay_chunk(replay.p, plan[c].first, plan[c].second, lmax, rs, st);
+            const cudaError_t ce3 = cudaStreamEndCapture(st, &gr);
+            CUDA_TRY(ce2);
+            CUDA_TRY(ce3);
+            const cudaError_t ce4 = cudaGraphInstantiate(part == 0 ? &rp_exec : &rp_exec2, gr, 0);
+            cudaGraphDestroy(gr);
+            CUDA_TRY(ce4);
+          }
           rp_m = m;
           rp_n = n;
           rp_lmax = lmax;
@@ -3980,6 +3992,23 @@ struct nnm_dataset {
           rp_state = rs;
         }
         CUDA_TRY(cudaGraphLaunch(rp_exec, st));
+        early_n = rp_split < nch ? plan[rp_split].first : m;
+        if (pin_out && early_n > 0) {
+          // records of the first part (final unless the GPU stopped there: then the host
+          // tail overwrites them after this copy has completed, see st2 below)
+          rec_dev.ensure(m);
+          CUDA_TRY(cudaEventRecord(ev2, st));
+          CUDA_TRY(cudaStreamWaitEvent(st2, ev2, 0));
+          merge_records_kernel<<<blocks_for(early_n), 256, 0, st2>>>(replay.p, early_n, r_rk.p,
+                                                                      r_rd.p, r_rs.p, rec_dev.p);
+          note_launch();
+          CUDA_TRY(cudaGetLastError());
+          CUDA_TRY(cudaMemcpyAsync(out, rec_dev.p, early_n * sizeof(nnm_merge),
+                                   cudaMemcpyDeviceToHost, st2));
+        } else {
+          early_n = 0;
+        }
+        if (rp_exec2) CUDA_TRY(cudaGraphLaunch(rp_exec2, st));
       } else {
         CUDA_TRY(replay_init(n, rs, st));
         DevBuf<int> cmax;
@@ -4016,13 +4045,15 @@ struct nnm_dataset {
                                    (m - host_from) * sizeof(ReplayEdge), cudaMemcpyDeviceToHost, st2));
         }
         // records [0, host_from) on the GPU, straight into the caller's page-locked array
-        if (host_from > 0) {
-          rec_dev.ensure(host_from);
-          merge_records_kernel<<<blocks_for(host_from), 256, 0, st>>>(replay.p, host_from, r_rk.p,
-                                                                      r_rd.p, r_rs.p, rec_dev.p);
+        // (the first early_n already on their way, above)
+        const int64_t r0 = std::min(early_n, host_from);
+        if (host_from > r0) {
+          rec_dev.ensure(m);
+          merge_records_kernel<<<blocks_for(host_from - r0), 256, 0, st>>>(
+              replay.p + r0, host_from - r0, r_rk.p + r0, r_rd.p + r0, r_rs.p + r0, rec_dev.p + r0);
           note_launch();
           CUDA_TRY(cudaGetLastError());
-          CUDA_TRY(cudaMemcpyAsync(out, rec_dev.p, host_from * sizeof(nnm_merge),
+          CUDA_TRY(cudaMemcpyAsync(out + r0, rec_dev.p + r0, (host_from - r0) * sizeof(nnm_merge),
                                    cudaMemcpyDeviceToHost, st));
         }
         rec_from = host_from;
