@@ -707,10 +707,13 @@ __global__ void __maxnreg__(128) tc_scan_kernel(TcArgs p) {
             }
           }
           if (ci >= 0 && b1 > -INFINITY) {
-            const double v1 = (double)__fmaf_rn(-2.f, b1, r);
-            const double e = (double)Erow * (1.0 + 1e-9) + 1.02 * 5.9604644775390625e-08 * fabs(v1);
-            const double up = sqrt(fmax(0.0, v1 + e)) * (1.0 + 1e-15) + (double)eta_row;
-            rowU = fminf(rowU, float_up(up * up * (1.0 + 1e-15)));
+            // the same bound as the seed's below, in fp32 with every step rounded up (a
+            // rigorous upper bound; the FP64 form cost a DSQRT per row and item)
+            const float v1 = __fmaf_rn(-2.f, b1, r);
+            const float e = __fmaf_ru(1.03f * 5.9604644775390625e-08f, fabsf(v1),
+                                      __fmul_ru(Erow, 1.000001f));
+            const float up = __fadd_ru(__fsqrt_ru(fmaxf(0.f, __fadd_ru(v1, e))), eta_row);
+            rowU = fminf(rowU, __fmul_ru(up, up));
           }
           gm = 0;  // no exact work in bound mode
         } else
