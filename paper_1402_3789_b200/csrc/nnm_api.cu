@@ -1861,10 +1861,13 @@ __global__ void cache_scatter_kernel(const int2* __restrict__ items, int64_t cnt
 // Phase-2 enumeration from the tile-pair bound table, appending the kept tile pairs as
 // u64 keys (I << 32 | J) with warp-aggregated atomics (unordered; sorted afterwards so
 // that every rank derives the identical list).  Same keep rule as enum_table_kernel.
+constexpr int CB = 8;  // tiles per side of a coarse bound block (coarse_min_kernel)
 __global__ void enum_append_kernel(const unsigned* __restrict__ bnd, const int2* __restrict__ trange,
                                    const double* __restrict__ umax, const unsigned* __restrict__ bits,
                                    int T, unsigned long long* __restrict__ out,
-                                   unsigned long long* __restrict__ count, unsigned long long cap) {
+                                   unsigned long long* __restrict__ count, unsigned long long cap,
+                                   const unsigned* __restrict__ cmin,
+                                   const double* __restrict__ bumax, int TB) {
   const int I = blockIdx.x;
   const int64_t w0 = tri_index(T, I, I);
   const int2 tI = trange[I];
@@ -1877,6 +1880,11 @@ __global__ void enum_append_kernel(const unsigned* __restrict__ bnd, const int2*
     for (int u = 0; u < U; ++u) {
       const int J = J0 + u * blockDim.x + threadIdx.x;
       k[u] = false;
+      // whole 8-tile blocks whose coarse bound already exceeds every component bound
+      // involved are skipped without touching the table (the pair test would drop them)
+      if (J < T && cmin &&
+          (double)__uint_as_float(cmin[(int64_t)(I / CB) * TB + J / CB]) > fmax(uI, bumax[J / CB]))
+        continue;
       if (J < T) {
         const int64_t w = w0 + (J - I);
         const int2 tJ = trange[J];
@@ -1902,6 +1910,34 @@ __global__ void enum_append_kernel(const unsigned* __restrict__ bnd, const int2*
       }
     }
   }
+}
+
+// Coarse bound table: per 8 x 8 block of tile pairs (I / 8, J / 8) the minimum of the
+// geometric bounds (uint order of non-negative fp32 bits), built once per dataset.  The
+// tile-pair cache only raises entries, so the block minimum stays a lower bound of every
+// entry the enumeration reads.
+__global__ void coarse_min_kernel(const unsigned* __restrict__ glb, int T, int TB,
+                                  unsigned* __restrict__ cmin) {
+  const int I = blockIdx.x;
+  const int64_t w0 = tri_index(T, I, I);
+  for (int J0 = I & ~(CB - 1); J0 < T; J0 += blockDim.x) {
+    const int J = J0 + threadIdx.x;  // blockDim a multiple of CB: lane groups align with blocks
+    unsigned v = (J >= I && J < T) ? glb[w0 + (J - I)] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int o = 1; o < CB; o <<= 1) v = min(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    if ((threadIdx.x & (CB - 1)) == 0 && J < T && v != 0xFFFFFFFFu)
+      atomicMin(cmin + (int64_t)(I / CB) * TB + J / CB, v);
+  }
+}
+
+// per block of CB tiles: the largest component bound (fmax: NaN ignored like the pair test)
+__global__ void block_umax_kernel(const double* __restrict__ umax, int T, int TB,
+                                  double* __restrict__ bumax) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= TB) return;
+  double m = -INFINITY;
+  for (int j = b * CB; j < min(T, (b + 1) * CB); ++j) m = fmax(m, umax[j]);
+  bumax[b] = m;
 }
 
 // sorted u64 item keys (I << 32 | J) -> int2 (I, J)
@@ -2557,6 +2593,10 @@ struct nnm_dataset {
   // per-dataset tile-pair tables (geom_metric): geometric lower bound per tile pair and
   // the NBR nearest tiles of every tile (phase-1 seed candidates)
   DevBuf<unsigned> glb;
+  DevBuf<unsigned> cmin;   // coarse block minima of glb (coarse_min_kernel)
+  DevBuf<double> bumax;    // per-round block maxima of the tile bounds
+  bool coarse_on = false;
+  int tb_ = 0;
   DevBuf<int> nbr;
   int glb_metric = -1, nbr_metric = -1;
   // per tile pair (triangle index): fp32 bits of a lower bound of S over its cross-component
@@ -3363,6 +3403,15 @@ struct nnm_dataset {
       note_launch();
       CUDA_TRY(cudaGetLastError());
       glb_metric = kind;
+      const char* ce = getenv("NNM_COARSE");
+      coarse_on = !(ce && ce[0] == '0');
+      if (coarse_on) {
+        tb_ = (Tp + CB - 1) / CB;
+        cmin.ensure((size_t)tb_ * tb_);
+        CUDA_TRY(cudaMemsetAsync(cmin.p, 0xFF, (size_t)tb_ * tb_ * sizeof(unsigned), st));
+        coarse_min_kernel<<<Tp, 256, 0, st>>>(glb.p, Tp, tb_, cmin.p); note_launch();
+        CUDA_TRY(cudaGetLastError());
+      }
     }
     if (on && (d == 25 || d == 8)) {
       p1_l.ensure((size_t)Tp * P1_CHUNKS * NBR_SLICE);
@@ -3441,8 +3490,13 @@ struct nnm_dataset {
       for (int attempt = 0; attempt < 2; ++attempt) {
         ekeys.ensure(cap);
         CUDA_TRY(cudaMemsetAsync(counters.p + 4, 0, sizeof(unsigned long long), st));
+        if (coarse_on && attempt == 0) {
+          bumax.ensure(tb_);
+          block_umax_kernel<<<blocks_for(tb_), 256, 0, st>>>(tumax.p, Tp, tb_, bumax.p); note_launch();
+        }
         enum_append_kernel<<<Tp, 256, 0, st>>>(tpmin_use ? tpmin.p : glb.p, tile_range.p, tumax.p,
-                                               pbits.p, Tp, ekeys.p, counters.p + 4, ekeys.n);
+                                               pbits.p, Tp, ekeys.p, counters.p + 4, ekeys.n,
+                                               coarse_on ? cmin.p : nullptr, bumax.p, tb_);
         note_launch();
         CUDA_TRY(cudaGetLastError());
         const unsigned long long cnt = read1(counters.p + 4);
