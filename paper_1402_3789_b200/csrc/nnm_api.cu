@@ -1947,13 +1947,14 @@ __global__ void keys_to_items_kernel(const unsigned long long* __restrict__ keys
   if (t < n) items[t] = make_int2((int)(keys[t] >> 32), (int)(keys[t] & 0xFFFFFFFFull));
 }
 
-// int2 (I <= J, or (-1, -1) padding) -> u64 key (padding ~0: sorts last)
+// int2 (I <= J, or (-1, -1) padding) -> u64 key (padding `pad` = (T << 32) | T: sorts last
+// and keeps the key inside the radix sort's bit range)
 __global__ void items_to_keys_kernel(const int2* __restrict__ items, int64_t n,
-                                     unsigned long long* __restrict__ keys) {
+                                     unsigned long long pad, unsigned long long* __restrict__ keys) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int2 it = items[t];
-  keys[t] = it.x < 0 ? ~0ull : (((unsigned long long)it.x << 32) | (unsigned)it.y);
+  keys[t] = it.x < 0 ? pad : (((unsigned long long)it.x << 32) | (unsigned)it.y);
 }
 
 __global__ void pos_caps_kernel(int64_t n, const int* __restrict__ comp,
@@ -3373,11 +3374,14 @@ struct nnm_dataset {
   // (I, J) items with (-1, -1) padding -> sorted unique items at the front; returns the count
   int64_t sort_unique_items(int2* items, int64_t n) {
     ekeys.ensure(n);
-    items_to_keys_kernel<<<blocks_for(n), 256, 0, st>>>(items, n, ekeys.p); note_launch();
-    sort_keys(ekeys.p, n, 32);  // all 64 bits: the ~0 padding must sort last
+    int pb = 1;  // bits of the row index, padding row Tp included
+    while (pb < 31 && ((int64_t)1 << pb) <= Tp) ++pb;
+    const unsigned long long pad = ((unsigned long long)Tp << 32) | (unsigned)Tp;
+    items_to_keys_kernel<<<blocks_for(n), 256, 0, st>>>(items, n, pad, ekeys.p); note_launch();
+    sort_keys(ekeys.p, n, pb);
     auto* end = thrust::unique(thrust::cuda::par(talloc).on(st), ekeys.p, ekeys.p + n);
     int64_t m = end - ekeys.p;
-    if (m > 0 && read1(ekeys.p + (m - 1)) == ~0ull) --m;
+    if (m > 0 && read1(ekeys.p + (m - 1)) == pad) --m;
     if (m > 0) { keys_to_items_kernel<<<blocks_for(m), 256, 0, st>>>(ekeys.p, m, items); note_launch(); }
     return m;
   }
