@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(256) small_boruvka_kernel(
 // R_i = norm(x_i) + max norm bounds norm(x_i) + norm(x_j) for every j.  Component minima,
 // hooking, root finding and relabelling follow as in small_boruvka_kernel, with the
 // pointer jumping replaced by a read-only walk to the root (one grid barrier).
-constexpr int SMALL_CW = 1024;       // columns per work unit
+constexpr int SMALL_CW = 2048;       // columns per work unit
 constexpr int SMALL_AUTO_N = 16384;  // default-on size limit (n^2 work per round)
 template <int M, int D, int R>
 __global__ void __launch_bounds__(256) small_screened_kernel(
