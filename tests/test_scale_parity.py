@@ -173,10 +173,13 @@ def test_c4_tensor_screen_equals_fp32_screen(nnm, c4):
 
 
 @pytest.mark.parametrize("env", [{"NNM_GPU_REPLAY": "0"}, {"NNM_REPLAY_LMAX": "4"},
-                                 {"NNM_REPLAY_CHUNKS": "700"}])
+                                 {"NNM_REPLAY_CHUNKS": "700"}, {"NNM_PINNED_OUT": "0"},
+                                 {"NNM_REPLAY_LMAX": "4", "NNM_PINNED_OUT": "0"}])
 def test_c4_gpu_replay_equals_host_replay(nnm, c4, env):
     """The component-parallel GPU replay == the sequential host replay at 2M (and the
-    mixed case where the GPU stops early and the host finishes)."""
+    mixed case where the GPU stops early and the host finishes), with the records laid
+    out by the GPU into page-locked outputs (default) or assembled on the host
+    (NNM_PINNED_OUT=0)."""
     a, ra = _run_digest(nnm, c4)
     b, rb = _run_digest(nnm, c4, **env)
     # the last chunk (inter-blob edges: one component) is finished on the host
