@@ -1240,9 +1240,12 @@ __global__ void tc_mirror_kernel(const int2* __restrict__ items, int64_t n,
       }
     }
     const unsigned long long db = (unsigned long long)__float_as_uint(dc);
-    keys[2 * w] = keep_ij ? ((unsigned long long)it.x << 32 | db) : ~0ull;
+    // dropped orientations: (T << 32 | ~0u) sorts after every kept key and stays inside the
+    // radix sort's bit range
+    const unsigned long long drop_key = ((unsigned long long)T << 32) | 0xFFFFFFFFull;
+    keys[2 * w] = keep_ij ? ((unsigned long long)it.x << 32 | db) : drop_key;
     js[2 * w] = it.y;
-    keys[2 * w + 1] = keep_ji ? ((unsigned long long)it.y << 32 | db) : ~0ull;
+    keys[2 * w + 1] = keep_ji ? ((unsigned long long)it.y << 32 | db) : drop_key;
     js[2 * w + 1] = it.x;
     drop = (keep_ij ? 0u : 1u) + (keep_ji ? 0u : 1u);
   }
@@ -2578,8 +2581,8 @@ struct nnm_dataset {
   bool tc_ready = false;
   DevBuf<float> tc_img, tc_tnorm, tc_eta, tc_meta, tc_sq;
   DevBuf<int2> tc_items;
-  DevBuf<unsigned long long> tc_keys;  // (I << 32 | centre-distance bits), radix-sorted
-  DevBuf<int> tc_js;
+  DevBuf<unsigned long long> tc_keys, tc_keys2;  // (I << 32 | centre-distance bits), sorted
+  DevBuf<int> tc_js, tc_js2;
   // dot form
   bool dot_on = false;
   DotModel dm{};
@@ -2878,7 +2881,22 @@ struct nnm_dataset {
                                                        tc_keys.p, tc_js.p,
                                                        counters.p + 5); note_launch();
     CUDA_TRY(cudaGetLastError());
-    thrust::sort_by_key(thrust::cuda::par(talloc).on(st), tc_keys.p, tc_keys.p + 2 * n_up, tc_js.p);
+    {  // radix sort over the bits the keys use (row tile incl. the drop row T, fp32 bits)
+      int pb = 1;
+      while (pb < 31 && ((int64_t)1 << pb) <= Tp) ++pb;
+      tc_keys2.ensure((size_t)2 * n_up);
+      tc_js2.ensure((size_t)2 * n_up);
+      size_t tb = 0;
+      CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, tc_keys.p, tc_keys2.p, tc_js.p, tc_js2.p,
+                                               (int)(2 * n_up), 0, 32 + pb, st));
+      sort_tmp.ensure(std::max<size_t>(tb, 1));
+      CUDA_TRY(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tb, tc_keys.p, tc_keys2.p, tc_js.p,
+                                               tc_js2.p, (int)(2 * n_up), 0, 32 + pb, st));
+      std::swap(tc_keys.p, tc_keys2.p);
+      std::swap(tc_keys.n, tc_keys2.n);
+      std::swap(tc_js.p, tc_js2.p);
+      std::swap(tc_js.n, tc_js2.n);
+    }
     const int64_t nfull = 2 * n_up - (int64_t)read1(counters.p + 5);
     tc_list_epoch = scan_epoch;
     tc_list_items = items;
