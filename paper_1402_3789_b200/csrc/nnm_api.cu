@@ -3993,7 +3993,7 @@ struct nnm_dataset {
       // join the blobs) is one component, so the host tail starts as late as possible
       std::vector<std::pair<int64_t, int>> plan;
       {
-        const int64_t C = std::max<int64_t>(4096, (m + nchunks - 1) / nchunks);
+        const int64_t C = std::max<int64_t>(32768, (m + nchunks - 1) / nchunks);
         const int64_t head_end = m - m / 8;
         int64_t lo = 0;
         while (lo < head_end) {
