@@ -223,8 +223,10 @@ def run_reference(args) -> None:
 
     X = config_dataset(CONFIGS[args.config][3])
     samples = []
+    # each step a bounded sample: the whole arm stays within ~2 minutes of CPU time
+    per_step = max(2.0, min(args.ref_seconds, 120.0 / max(1, args.warmup + args.steps)))
     for step in range(args.warmup + args.steps):
-        cb = cpu_baseline(X, seconds_target=args.ref_seconds, cfg_name=args.config)
+        cb = cpu_baseline(X, seconds_target=per_step, cfg_name=args.config)
         if step >= args.warmup:
             samples.append(cb)
     v = statistics.median(s["value"] for s in samples)
