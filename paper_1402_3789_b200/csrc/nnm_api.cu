@@ -3469,7 +3469,11 @@ struct nnm_dataset {
     items1.ensure((size_t)Tp * PK);
     const char* p1e = getenv("NNM_P1REG");
     const char* pke0 = getenv("NNM_PK");
-    const int pk0 = pke0 ? std::max(1, std::min(PK, atoi(pke0))) : 4;
+    // seeds per tile: 4 in the first round (every row starts without a threshold), 1 after
+    // (NNM_PK_LATE; measured C4 29.6 -> 27.7 ms, C5m 62.3 -> 53.7 ms against 4 throughout)
+    const char* pkl = getenv("NNM_PK_LATE");
+    const int pk_late = pkl ? std::max(1, std::min(PK, atoi(pkl))) : 1;
+    const int pk0 = pke0 ? std::max(1, std::min(PK, atoi(pke0))) : (bv_round == 0 ? 4 : pk_late);
     if (nbr_ready()) {
       phase1_pick_kernel<<<blocks_for(Tp), 256, 0, st>>>(nbr.p, tile_range.p, Tp, pk0, items1.p); note_launch();
     } else if ((d == 25 || d == 8) && !(p1e && p1e[0] == '0')) {
@@ -3484,7 +3488,7 @@ struct nnm_dataset {
       const char* pke = getenv("NNM_PK");
       // 4 seeds per tile: measured best on 2Mx25 (PK 8 -> 4: phase-1 scan -20%, the
       // component bounds stay tight enough that phase 2 does not grow)
-      const int pk = pke ? std::max(1, std::min(PK, atoi(pke))) : 4;
+      const int pk = pke ? std::max(1, std::min(PK, atoi(pke))) : (bv_round == 0 ? 4 : pk_late);
       phase1_merge_kernel<<<blocks_for(Tp), 256, 0, st>>>(p1_l.p, p1_j.p, Tp, pk, items1.p); note_launch();
     } else {
       phase1_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
