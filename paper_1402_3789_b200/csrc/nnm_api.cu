@@ -3473,7 +3473,9 @@ struct nnm_dataset {
     // (NNM_PK_LATE; measured C4 29.6 -> 27.7 ms, C5m 62.3 -> 53.7 ms against 4 throughout)
     const char* pkl = getenv("NNM_PK_LATE");
     const int pk_late = pkl ? std::max(1, std::min(PK, atoi(pkl))) : 1;
-    const int pk0 = pke0 ? std::max(1, std::min(PK, atoi(pke0))) : (bv_round == 0 ? 4 : pk_late);
+    const char* pkf = getenv("NNM_PK_FIRST");
+    const int pk_first = pkf ? std::max(1, std::min(PK, atoi(pkf))) : 4;
+    const int pk0 = pke0 ? std::max(1, std::min(PK, atoi(pke0))) : (bv_round == 0 ? pk_first : pk_late);
     if (nbr_ready()) {
       phase1_pick_kernel<<<blocks_for(Tp), 256, 0, st>>>(nbr.p, tile_range.p, Tp, pk0, items1.p); note_launch();
     } else if ((d == 25 || d == 8) && !(p1e && p1e[0] == '0')) {
@@ -3488,7 +3490,7 @@ struct nnm_dataset {
       const char* pke = getenv("NNM_PK");
       // 4 seeds per tile: measured best on 2Mx25 (PK 8 -> 4: phase-1 scan -20%, the
       // component bounds stay tight enough that phase 2 does not grow)
-      const int pk = pke ? std::max(1, std::min(PK, atoi(pke))) : (bv_round == 0 ? 4 : pk_late);
+      const int pk = pke ? std::max(1, std::min(PK, atoi(pke))) : (bv_round == 0 ? pk_first : pk_late);
       phase1_merge_kernel<<<blocks_for(Tp), 256, 0, st>>>(p1_l.p, p1_j.p, Tp, pk, items1.p); note_launch();
     } else {
       phase1_kernel<M><<<(Tp + TR - 1) / TR, 256, 0, st>>>(tc32.p, tr32.p, tile_range.p, Tp, d, items1.p); note_launch();
