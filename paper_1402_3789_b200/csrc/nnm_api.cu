@@ -4284,7 +4284,7 @@ struct nnm_dataset {
   // reuse (rounds of one run): eligibility only shrinks as clusters merge, so the rB1 of
   // an earlier snapshot still bounds every eligible partner from below and its row-best
   // pairs that are still eligible are real candidates: the full scan is skipped until
-  // A grows past n/8 (or fewer than P row-best pairs survive) -- SURVEY 8(f) rank 2.
+  // A grows past n/6 (NNM_REUSE_DIV; or fewer than P row-best pairs survive) -- SURVEY 8(f) rank 2.
   bool top_p_pass(int metric, double thr, int kl2, int kl3, int64_t P, const int* psz, int ksum,
                   int64_t max_active, std::vector<Cand>& out) {
     counters.ensure(8);
@@ -4335,7 +4335,9 @@ struct nnm_dataset {
     const char* re = getenv("NNM_ROUND_REUSE");
     if (reuse && rb1_valid && !(re && re[0] == '0')) {
       const int* psz = ksum != INT_UNSET ? eff_sizes(kl2) : comp.p;
-      if (top_p_pass(metric, thr, kl2, kl3, P, psz, ksum, std::max<int64_t>(2 * P, n / 8), out))
+      const char* rfe = getenv("NNM_REUSE_DIV");  // reuse while |A| <= n / div
+      const int64_t div = rfe ? std::max(1, atoi(rfe)) : 6;  // C2 sweep: 4 528, 6 474, 8 491, 11 554 ms
+      if (top_p_pass(metric, thr, kl2, kl3, P, psz, ksum, std::max<int64_t>(2 * P, n / div), out))
         return;
       ++stats.round_rescans;
     }
